@@ -1,0 +1,226 @@
+/*
+ * cbaa.h — C ABI of the B200-native CBAA window path (libcbaa.so).
+ *
+ * CBAA = "Cube of Bits Array Algorithm" of Xu, Ding, Hu, "GPU based Real-time
+ * Super Hosts Detection at Distributed Edge Routers" (arXiv 1901.06207).
+ * Citations: "P:n" = line n of the paper text, "S:n" = line n of
+ * SPEC.md, "Qn" = reading n of DESIGN.md §3.
+ *
+ * Problem statement: the pairs <inner ip, outer ip> of a
+ * time window go in; the inner hosts with at least θ distinct opposite IPs
+ * (super hosts, Def. 1) come out.  One handle = one local server's cube of
+ * bits arrays (CBA) on one GPU.  Per window the caller does
+ *     cbaa_reset → cbaa_update* → [cbaa_merge*] → cbaa_detect.
+ *
+ * Conventions for every entry point:
+ *  - Return value: CBAA_OK (0) or a negative CBAA_E_* code; never throws.
+ *    cbaa_last_error(h) holds a one-line explanation of the last failure.
+ *  - Pointers named "device" are CUDA device pointers on the handle's device;
+ *    "host" pointers are ordinary (optionally pinned) host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are asynchronous and stream-ordered unless documented otherwise;
+ *    the caller keeps every buffer it passes alive until `stream` completes.
+ *  - IPv4 addresses are host-order uint32 (192.168.1.1 = 0xC0A80101, Q31).
+ *  - A handle is single-stream and not thread-safe; distinct handles are
+ *    independent (k handles on one GPU simulate k edge routers).
+ *
+ * Memory layout of the cube (Q27): CSs ascending; inside a CS the
+ * arrays RA(0..num_ra-1) then VA(0..num_va-1); inside an array the columns
+ * ascending; inside a column the g rows, row j = bit (j mod 32) of 32-bit word
+ * j/32 (little-endian), i.e. bit (j mod 8) of byte j/8 — the SPEC's byte format.
+ */
+#ifndef CBAA_H_
+#define CBAA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBAA_MAX_RA 8
+#define CBAA_MAX_VA 8
+#define CBAA_MAX_ARRAYS 16
+#define CBAA_MAX_PREFIXES 16
+#define CBAA_MAX_MERGE 64
+
+/* Status codes. */
+#define CBAA_OK 0
+#define CBAA_E_CONFIG (-1)    /* config violates an invariant of S:37-41; last_error names it */
+#define CBAA_E_ARG (-2)       /* null / misaligned pointer, bad range, wrong device               */
+#define CBAA_E_CUDA (-3)      /* a CUDA call failed; last_error carries cudaGetErrorString         */
+#define CBAA_E_MISMATCH (-4)  /* merge of cubes that are not the same size                 */
+#define CBAA_E_CAPACITY (-5)  /* more hosts than `cap`: *n_out = required count, out = first cap  */
+#define CBAA_E_TUPLE_CAP (-6) /* ≥1 CS skipped: ∏|HC(i)| > tuple_cap; others still output */
+#define CBAA_E_NOMEM (-7)     /* device allocation failed                                         */
+
+#define CBAA_THETA_PAPER 0    /* θ_bn = g(1+ε)e^{−θ/g} − gε, P:261 (default)                     */
+#define CBAA_THETA_INVERTED 1 /* θ_bn = g(1−ε)e^{−θ/g}, Theorem 2 inverted (Q15)           */
+
+#define CBAA_DIR_NORMALIZED 0   /* src = inner, dst = outer as given (Q25)                 */
+#define CBAA_DIR_INNER_PREFIX 1 /* classify by inner prefixes; swap or skip              */
+
+typedef void* cbaa_stream; /* cudaStream_t */
+typedef struct cbaa_handle cbaa_handle;
+
+/* Sketch geometry and seeds (SketchConfig).  Invariants checked by
+ * cbaa_config_validate: 1 ≤ r ≤ 16 (or 0); 2 ≤ num_ra ≤ 8; num_va ≤ 8;
+ * g a power of two ≥ 32 (Q28); mangle_a odd; 1 ≤ cbn(i) ≤ min(32−r, 24);
+ * clbs strictly increasing and < L = 32−r (Q6); Σ|EP(i)| = L; 0 ≤ |CP(i)| ≤
+ * |EP((i+1) mod num_ra)|; cube ≤ 16 GiB. */
+typedef struct {
+  uint32_t r;                          /* right bits of the mangled inner IP selecting the CS */
+  uint32_t num_ra, num_va;             /* |RA|, |VA|                                            */
+  uint32_t g;                          /* rows (bits) per column                                */
+  uint8_t cbn[CBAA_MAX_ARRAYS];        /* c(i) = 2^cbn(i) columns of array i (Q9)                */
+  uint8_t clbs[CBAA_MAX_RA];           /* CL_bs(i): LP-relative, MSB-first start offsets (Q6, Q7)       */
+  uint32_t mangle_a, mangle_b;         /* mangle(x) = a·x + b mod 2^32, a odd (Q3)               */
+  uint32_t bv_seed;                    /* row hash H_bv = mix32(mangled oip ⊕ bv_seed) (Q2, Q4)  */
+  uint32_t va_seeds[CBAA_MAX_VA];      /* H_j = mix32(LP ⊕ va_seeds[j]) (Q4, Q10)                */
+  int32_t theta_formula;               /* CBAA_THETA_PAPER | CBAA_THETA_INVERTED                         */
+  int32_t direction;                   /* CBAA_DIR_NORMALIZED | CBAA_DIR_INNER_PREFIX                    */
+  uint64_t tuple_cap;                  /* per-CS cap on ∏|HC(i)|, default 2^24                   */
+  uint32_t n_prefixes;                 /* inner prefixes used with CBAA_DIR_INNER_PREFIX                 */
+  uint32_t inner_prefix[CBAA_MAX_PREFIXES];
+  uint32_t inner_mask[CBAA_MAX_PREFIXES]; /* ip is inner iff (ip & mask[k]) == prefix[k] for some k      */
+  uint32_t update_passes;              /* address-range passes of the update (0 = auto)   */
+  uint32_t hit_capacity;               /* device hit buffer entries per detect (0 = 2^20)               */
+  uint32_t reserved[6];
+} cbaa_config;
+
+/* One restored super host (Alg. 3 output). */
+typedef struct {
+  uint32_t ip;       /* original inner IP = unmangle((lp << r) | cs) */
+  uint32_t cs;       /* CS index = RP                                               */
+  uint32_t lp;       /* restored left part                                  */
+  uint32_t z;        /* zero bits of the union column (Def. 2)               */
+  double estimate;   /* −g·ln(Z/(g−g·ε)) (Thm. 2); +inf if Z = 0 (Q21)      */
+} cbaa_host;
+
+/* Per-CS window statistics of a detect. */
+typedef struct {
+  uint64_t ztot;          /* zero bits of RA(0) of the CS (η source, Q12)                 */
+  double eta;             /* −c0·g·ln(ztot/(c0·g)); +inf if ztot = 0                        */
+  double eps;             /* Theorem 1 over all arrays, capped at 1−2^−20   */
+  double theta_bn;        /* zero-bit threshold (P:261 or Q15), clamped ≥ 0                 */
+  uint32_t zmax;          /* ⌊θ_bn⌋ clamped to [0, g]: accept iff Z ≤ zmax (Q16)            */
+  uint32_t n_hot[CBAA_MAX_RA]; /* |HC(i)| (Alg. 2)                                          */
+  uint64_t tuples;        /* ∏|HC(i)| (saturating)                                          */
+  uint64_t candidates;    /* tuples passing the CP check (Alg. 3)                 */
+  uint64_t hits;          /* candidates accepted by the union-column test           */
+  int32_t overflow;       /* 1: tuples > tuple_cap, CS skipped                      */
+  int32_t _pad;
+} cbaa_cs_stats;
+
+/* ---------------------------------------------------------------- host only
+ * These three need no GPU. */
+
+/* Paper geometry (r=4, |RA|=3, |VA|=1, g=c=2^12) with clbs = [0,10,20]
+ * (Q8) and the seeds of Q3/Q4; θ formula = paper; tuple_cap = 2^24. */
+int cbaa_config_default(cbaa_config* out);
+
+/* Checks every invariant above.  On failure returns CBAA_E_CONFIG and writes
+ * the violated rule into err (errlen bytes, NUL-terminated) when non-null. */
+int cbaa_config_validate(const cbaa_config* cfg, char* err, uint64_t errlen);
+
+/* Cube size 2^r·Σ_i c(i)·g/8 bytes; 0 for an invalid config. */
+uint64_t cbaa_cube_bytes(const cbaa_config* cfg);
+
+/* ----------------------------------------------------------------- lifetime */
+
+/* Validates cfg, selects `device`, allocates the cube (zeroed) and all detect
+ * scratch.  *out owns everything until cbaa_destroy. */
+int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out);
+void cbaa_destroy(cbaa_handle* h);
+int cbaa_get_config(const cbaa_handle* h, cbaa_config* out);
+
+/* Window reset: cube := 0 (implicit per window). Async on stream. */
+int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
+
+/* ------------------------------------------------------------------- update */
+
+/* Alg. 1 for n pairs: src[k], dst[k] are DEVICE arrays of
+ * host-order IPv4 (src = inner, dst = outer unless direction = INNER_PREFIX).
+ * Sets |RA|+|VA| bits per pair with 32-bit atomic OR (Q11).  Any alignment is
+ * accepted (16-B aligned arrays take the vector path).  Async on stream. */
+int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream);
+
+/* Same as cbaa_update for HOST arrays (pinned or pageable): the library copies
+ * them to the device in chunks on its own copy stream, double-buffered and
+ * overlapped with the update kernels (the local-server buffer → GPU copy of
+ * P:338).  Returns after every copy has been enqueued; stream-ordered. */
+int cbaa_update_host(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream);
+
+/* Pairs dropped by the INNER_PREFIX classification since the last reset
+ * (zero or two inner endpoints).  Synchronizes stream. */
+int cbaa_skipped(cbaa_handle* h, uint64_t* out, cbaa_stream stream);
+
+/* -------------------------------------------------------------------- merge */
+
+/* Global merge by bitwise OR (Q1): cube |= cubes[0] | … | cubes[k−1].
+ * Each cubes[j] is a DEVICE pointer to a full cube of identical geometry
+ * (nbytes must equal cbaa_cube_bytes; the caller checks seed identity).
+ * k ≤ CBAA_MAX_MERGE.  Peer pointers are allowed. Async on stream. */
+int cbaa_merge(cbaa_handle* h, const void* const* cubes, int k, uint64_t nbytes, cbaa_stream stream);
+
+/* Merge of a CS range only: slices[j] points at the bytes of CSs
+ * [cs_lo, cs_hi) of a cube of identical geometry (contiguous, CS-aligned).
+ * Used when each rank owns a CS range. Async on stream. */
+int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
+                     cbaa_stream stream);
+
+/* ------------------------------------------------------------------- detect */
+
+/* Window end over every CS: zero counts → η, ε, θ_bn, zmax per CS
+ * → hot columns (Alg. 2) → tuple CP-join and union-column check (Alg. 3) →
+ * hosts sorted by estimate descending then ip ascending.
+ * out: HOST array of `cap` entries; *n_out = number of hosts found.
+ * stats: HOST array of 2^r entries, or NULL.  SYNCHRONIZES stream.
+ * Returns CBAA_E_CAPACITY if *n_out > cap, CBAA_E_TUPLE_CAP if a CS overflowed
+ * (both still fill out/stats). */
+int cbaa_detect(cbaa_handle* h, uint32_t theta, cbaa_host* out, uint64_t cap, uint64_t* n_out,
+                cbaa_cs_stats* stats, cbaa_stream stream);
+
+/* Same restricted to CSs [cs_lo, cs_hi); stats then holds cs_hi − cs_lo entries. */
+int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t cs_hi, cbaa_host* out,
+                      uint64_t cap, uint64_t* n_out, cbaa_cs_stats* stats, cbaa_stream stream);
+
+/* ---------------------------------------------------------------- inspection */
+
+/* Device pointer and size of the cube (for NCCL exchange and parity dumps). */
+int cbaa_cube_view(cbaa_handle* h, void** dev_ptr, uint64_t* nbytes);
+
+/* Zero count of every RA column (Alg. 2 input), DEVICE out of
+ * 2^r·Σ_{i<num_ra} c(i) uint32 in the order cs → RA(i) → column.  Async. */
+int cbaa_zero_counts(cbaa_handle* h, uint32_t* out, cbaa_stream stream);
+
+/* After a detect: HOST copies of the hot-column lists (per CS, per RA(i),
+ * ascending; counts in stats.n_hot) — `out` holds 2^r·Σ c(i) entries laid
+ * out like cbaa_zero_counts with each (cs, i) block's first n_hot entries
+ * valid.  Synchronizes stream. */
+int cbaa_hot_columns(cbaa_handle* h, uint32_t* out, cbaa_stream stream);
+
+/* Record candidate LPs during the next detects (debug; costs one atomic per
+ * candidate).  cbaa_candidates copies (cs << 32 | lp) of the last detect into
+ * a HOST array of cap entries, unordered; *n_out = total.  Synchronizes. */
+int cbaa_set_record_candidates(cbaa_handle* h, int enable, uint64_t capacity);
+int cbaa_candidates(cbaa_handle* h, uint64_t* out, uint64_t cap, uint64_t* n_out, cbaa_stream stream);
+
+/* Test-only: the device-side mapping of Alg. 1 for n pairs (DEVICE arrays):
+ * cs[k], cols[k·(num_ra+num_va) + a], row[k].  Async on stream. */
+int cbaa_debug_map(cbaa_handle* h, const uint32_t* iip, const uint32_t* oip, uint64_t n, uint32_t* cs,
+                   uint32_t* cols, uint32_t* row, cbaa_stream stream);
+
+/* Number of kernels this handle has launched since creation (bench evidence). */
+uint64_t cbaa_kernel_launches(const cbaa_handle* h);
+
+/* Update passes the handle uses (resolved from update_passes = 0). */
+uint32_t cbaa_update_passes(const cbaa_handle* h);
+
+const char* cbaa_strerror(int code);
+const char* cbaa_last_error(const cbaa_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBAA_H_ */

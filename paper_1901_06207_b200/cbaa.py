@@ -1,0 +1,344 @@
+"""Thin Python binding of libcbaa.so (include/cbaa.h): argument marshalling only.
+
+Every step of the window path runs in the library's sm_100a kernels; this module
+only converts torch tensors / numpy arrays into pointers, sizes and the current
+CUDA stream.  If the library is missing the import fails loudly — there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcbaa.so")
+
+MAX_RA, MAX_VA, MAX_ARRAYS, MAX_PREFIXES = 8, 8, 16, 16
+
+OK = 0
+E_CONFIG, E_ARG, E_CUDA, E_MISMATCH, E_CAPACITY, E_TUPLE_CAP, E_NOMEM = -1, -2, -3, -4, -5, -6, -7
+THETA_PAPER, THETA_INVERTED = 0, 1
+DIR_NORMALIZED, DIR_INNER_PREFIX = 0, 1
+
+
+class Config(C.Structure):
+    """cbaa_config (include/cbaa.h)."""
+    _fields_ = [
+        ("r", C.c_uint32), ("num_ra", C.c_uint32), ("num_va", C.c_uint32), ("g", C.c_uint32),
+        ("cbn", C.c_uint8 * MAX_ARRAYS), ("clbs", C.c_uint8 * MAX_RA),
+        ("mangle_a", C.c_uint32), ("mangle_b", C.c_uint32), ("bv_seed", C.c_uint32),
+        ("va_seeds", C.c_uint32 * MAX_VA),
+        ("theta_formula", C.c_int32), ("direction", C.c_int32), ("tuple_cap", C.c_uint64),
+        ("n_prefixes", C.c_uint32), ("inner_prefix", C.c_uint32 * MAX_PREFIXES),
+        ("inner_mask", C.c_uint32 * MAX_PREFIXES), ("update_passes", C.c_uint32), ("hit_capacity", C.c_uint32),
+        ("reserved", C.c_uint32 * 6),
+    ]
+
+    def to_dict(self) -> dict:
+        n = self.num_ra + self.num_va
+        return dict(r=self.r, num_ra=self.num_ra, num_va=self.num_va, g=self.g, cbn=list(self.cbn[:n]),
+                    clbs=list(self.clbs[: self.num_ra]), mangle_a=self.mangle_a, mangle_b=self.mangle_b,
+                    bv_seed=self.bv_seed, va_seeds=list(self.va_seeds[: self.num_va]),
+                    theta_formula=self.theta_formula, tuple_cap=self.tuple_cap, direction=self.direction,
+                    prefixes=[(self.inner_prefix[k], self.inner_mask[k]) for k in range(self.n_prefixes)])
+
+
+class Host(C.Structure):
+    _fields_ = [("ip", C.c_uint32), ("cs", C.c_uint32), ("lp", C.c_uint32), ("z", C.c_uint32),
+                ("estimate", C.c_double)]
+
+
+class CsStats(C.Structure):
+    _fields_ = [("ztot", C.c_uint64), ("eta", C.c_double), ("eps", C.c_double), ("theta_bn", C.c_double),
+                ("zmax", C.c_uint32), ("n_hot", C.c_uint32 * MAX_RA), ("tuples", C.c_uint64),
+                ("candidates", C.c_uint64), ("hits", C.c_uint64), ("overflow", C.c_int32), ("_pad", C.c_int32)]
+
+
+HOST_DTYPE = np.dtype([("ip", "<u4"), ("cs", "<u4"), ("lp", "<u4"), ("z", "<u4"), ("estimate", "<f8")])
+
+# Every entry point of include/cbaa.h with its ctypes signature.
+_P = C.POINTER
+_h = C.c_void_p
+_SIGS = {
+    "cbaa_config_default": (C.c_int, [_P(Config)]),
+    "cbaa_config_validate": (C.c_int, [_P(Config), C.c_char_p, C.c_uint64]),
+    "cbaa_cube_bytes": (C.c_uint64, [_P(Config)]),
+    "cbaa_create": (C.c_int, [_P(Config), C.c_int, _P(C.c_void_p)]),
+    "cbaa_destroy": (None, [_h]),
+    "cbaa_get_config": (C.c_int, [_h, _P(Config)]),
+    "cbaa_reset": (C.c_int, [_h, C.c_void_p]),
+    "cbaa_update": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "cbaa_update_host": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "cbaa_skipped": (C.c_int, [_h, _P(C.c_uint64), C.c_void_p]),
+    "cbaa_merge": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_uint64, C.c_void_p]),
+    "cbaa_merge_slice": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "cbaa_detect": (C.c_int, [_h, C.c_uint32, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p, C.c_void_p]),
+    "cbaa_detect_range": (C.c_int, [_h, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64,
+                                    _P(C.c_uint64), C.c_void_p, C.c_void_p]),
+    "cbaa_cube_view": (C.c_int, [_h, _P(C.c_void_p), _P(C.c_uint64)]),
+    "cbaa_zero_counts": (C.c_int, [_h, C.c_void_p, C.c_void_p]),
+    "cbaa_hot_columns": (C.c_int, [_h, C.c_void_p, C.c_void_p]),
+    "cbaa_set_record_candidates": (C.c_int, [_h, C.c_int, C.c_uint64]),
+    "cbaa_candidates": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
+    "cbaa_debug_map": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
+    "cbaa_kernel_launches": (C.c_uint64, [_h]),
+    "cbaa_update_passes": (C.c_uint32, [_h]),
+    "cbaa_strerror": (C.c_char_p, [C.c_int]),
+    "cbaa_last_error": (C.c_char_p, [_h]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libcbaa.so (built by __graft_entry__.build()); raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+class CbaaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{msg} (code {code}: {lib().cbaa_strerror(code).decode()})")
+        self.code = code
+
+
+def default_config() -> Config:
+    c = Config()
+    lib().cbaa_config_default(C.byref(c))
+    return c
+
+
+def config_from_dict(p: dict) -> Config:
+    """Build a cbaa_config from a plain parameter dict (the SPEC's field names)."""
+    c = default_config()
+    c.r, c.num_ra, c.num_va, c.g = p["r"], p["num_ra"], p["num_va"], p["g"]
+    for i in range(MAX_ARRAYS):
+        c.cbn[i] = p["cbn"][i] if i < len(p["cbn"]) else 0
+    for i in range(MAX_RA):
+        c.clbs[i] = p["clbs"][i] if i < len(p["clbs"]) else 0
+    c.mangle_a, c.mangle_b, c.bv_seed = p["mangle_a"], p["mangle_b"], p["bv_seed"]
+    for j in range(MAX_VA):
+        c.va_seeds[j] = p["va_seeds"][j] if j < len(p["va_seeds"]) else 0
+    c.theta_formula = p.get("theta_formula", THETA_PAPER)
+    c.tuple_cap = p.get("tuple_cap", 1 << 24)
+    c.direction = p.get("direction", DIR_NORMALIZED)
+    prefixes = p.get("prefixes", [])
+    c.n_prefixes = len(prefixes)
+    for k, (pre, mask) in enumerate(prefixes):
+        c.inner_prefix[k], c.inner_mask[k] = pre, mask
+    c.update_passes = p.get("update_passes", 0)
+    c.hit_capacity = p.get("hit_capacity", 0)
+    return c
+
+
+def validate(cfg: Config):
+    buf = C.create_string_buffer(256)
+    rc = lib().cbaa_config_validate(C.byref(cfg), buf, 256)
+    return rc, buf.value.decode()
+
+
+def cube_bytes(cfg: Config) -> int:
+    return lib().cbaa_cube_bytes(C.byref(cfg))
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA tensor")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError(f"{what} must be int32/uint32 (IPv4 as 32-bit words), got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+class Cbaa:
+    """One cube of bits arrays on one GPU (a local server's CBA)."""
+
+    def __init__(self, cfg: Config | dict | None = None, device: int = 0):
+        if cfg is None:
+            cfg = default_config()
+        elif isinstance(cfg, dict):
+            cfg = config_from_dict(cfg)
+        self.cfg = cfg
+        self.device = device
+        h = C.c_void_p()
+        rc = lib().cbaa_create(C.byref(cfg), device, C.byref(h))
+        if rc != OK:
+            raise CbaaError(rc, "cbaa_create failed: " + validate(cfg)[1])
+        self._h = h
+        self.n_cs = 1 << cfg.r
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().cbaa_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what, allow=()):
+        if rc != OK and rc not in allow:
+            raise CbaaError(rc, f"{what}: {lib().cbaa_last_error(self._h).decode()}")
+        return rc
+
+    # ---------------------------------------------------------------- window ops
+    def reset(self, stream=None):
+        self._check(lib().cbaa_reset(self._h, _stream(stream)), "cbaa_reset")
+
+    def update(self, src, dst, stream=None):
+        """Alg. 1 over device tensors src (inner) / dst (outer)."""
+        if src.numel() != dst.numel():
+            raise ValueError("src and dst differ in length")
+        self._check(lib().cbaa_update(self._h, _dptr(src, "src"), _dptr(dst, "dst"), src.numel(), _stream(stream)),
+                    "cbaa_update")
+
+    def update_host(self, src, dst, stream=None):
+        """Alg. 1 over HOST arrays (numpy or CPU tensors, ideally pinned): pipelined H2D inside the library."""
+        import torch
+        ps, pd = [], []
+        for a, lst in ((src, ps), (dst, pd)):
+            if isinstance(a, torch.Tensor):
+                if a.is_cuda or not a.is_contiguous() or a.element_size() != 4:
+                    raise TypeError("update_host needs contiguous 32-bit CPU tensors")
+                lst.append(a.data_ptr())
+            else:
+                a = np.ascontiguousarray(a)
+                if a.dtype.itemsize != 4:
+                    raise TypeError("update_host needs 32-bit arrays")
+                lst.append(a.ctypes.data)
+        n = len(src)
+        self._check(lib().cbaa_update_host(self._h, C.c_void_p(ps[0]), C.c_void_p(pd[0]), n, _stream(stream)),
+                    "cbaa_update_host")
+
+    def skipped(self, stream=None) -> int:
+        v = C.c_uint64()
+        self._check(lib().cbaa_skipped(self._h, C.byref(v), _stream(stream)), "cbaa_skipped")
+        return v.value
+
+    def merge(self, cubes, stream=None):
+        """cube |= OR of the given device cubes (uint8 tensors of cube_bytes, or other Cbaa handles)."""
+        ptrs = [(c.cube_ptr() if isinstance(c, Cbaa) else c.data_ptr()) for c in cubes]
+        arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+        self._check(lib().cbaa_merge(self._h, arr, len(ptrs), self.nbytes, _stream(stream)), "cbaa_merge")
+
+    def merge_slice(self, slices, cs_lo, cs_hi, stream=None):
+        ptrs = [s.data_ptr() for s in slices]
+        arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+        self._check(lib().cbaa_merge_slice(self._h, arr, len(ptrs), cs_lo, cs_hi, _stream(stream)),
+                    "cbaa_merge_slice")
+
+    def detect(self, theta: int, cap: int = 1 << 20, cs_lo: int = 0, cs_hi: int | None = None, stream=None,
+               raise_on_overflow: bool = False):
+        """Window end: returns (hosts structured array, per-CS stats list, status code)."""
+        cs_hi = self.n_cs if cs_hi is None else cs_hi
+        out = np.zeros(max(cap, 1), dtype=HOST_DTYPE)
+        stats = (CsStats * (cs_hi - cs_lo))()
+        n = C.c_uint64()
+        rc = lib().cbaa_detect_range(self._h, theta, cs_lo, cs_hi, out.ctypes.data_as(C.c_void_p), cap,
+                                     C.byref(n), stats, _stream(stream))
+        allow = () if raise_on_overflow else (E_TUPLE_CAP,)
+        self._check(rc, "cbaa_detect", allow=allow)
+        hosts = out[: min(n.value, cap)].copy()
+        sd = [dict(ztot=s.ztot, eta=s.eta, eps=s.eps, theta_bn=s.theta_bn, zmax=s.zmax,
+                   n_hot=list(s.n_hot[: self.cfg.num_ra]), tuples=s.tuples, candidates=s.candidates, hits=s.hits,
+                   overflow=s.overflow) for s in stats]
+        return hosts, sd, rc
+
+    # ---------------------------------------------------------------- inspection
+    @property
+    def nbytes(self) -> int:
+        p, n = C.c_void_p(), C.c_uint64()
+        self._check(lib().cbaa_cube_view(self._h, C.byref(p), C.byref(n)), "cbaa_cube_view")
+        return n.value
+
+    def cube_ptr(self) -> int:
+        p, n = C.c_void_p(), C.c_uint64()
+        self._check(lib().cbaa_cube_view(self._h, C.byref(p), C.byref(n)), "cbaa_cube_view")
+        return p.value
+
+    def cube(self):
+        """The device cube as a torch.uint8 tensor view (no copy; valid while the handle lives)."""
+        import torch
+        p, n = C.c_void_p(), C.c_uint64()
+        self._check(lib().cbaa_cube_view(self._h, C.byref(p), C.byref(n)), "cbaa_cube_view")
+        return _wrap_device(p.value, n.value, self.device, self)
+
+    def zero_counts(self, stream=None):
+        import torch
+        n = self.n_cs * sum(1 << self.cfg.cbn[i] for i in range(self.cfg.num_ra))
+        out = torch.empty(n, dtype=torch.int32, device=f"cuda:{self.device}")
+        self._check(lib().cbaa_zero_counts(self._h, C.c_void_p(out.data_ptr()), _stream(stream)), "cbaa_zero_counts")
+        return out
+
+    def hot_columns(self, stream=None) -> np.ndarray:
+        n = self.n_cs * sum(1 << self.cfg.cbn[i] for i in range(self.cfg.num_ra))
+        out = np.zeros(n, dtype=np.uint32)
+        self._check(lib().cbaa_hot_columns(self._h, out.ctypes.data_as(C.c_void_p), _stream(stream)),
+                    "cbaa_hot_columns")
+        return out
+
+    def record_candidates(self, enable=True, capacity=1 << 22):
+        self._check(lib().cbaa_set_record_candidates(self._h, int(enable), capacity), "cbaa_set_record_candidates")
+
+    def candidates(self, cap=1 << 22, stream=None) -> np.ndarray:
+        out = np.zeros(cap, dtype=np.uint64)
+        n = C.c_uint64()
+        self._check(lib().cbaa_candidates(self._h, out.ctypes.data_as(C.c_void_p), cap, C.byref(n), _stream(stream)),
+                    "cbaa_candidates")
+        return out[: min(n.value, cap)]
+
+    def debug_map(self, iip, oip, stream=None):
+        import torch
+        n = iip.numel()
+        narr = self.cfg.num_ra + self.cfg.num_va
+        dev = iip.device
+        cs = torch.empty(n, dtype=torch.int32, device=dev)
+        cols = torch.empty(n * narr, dtype=torch.int32, device=dev)
+        row = torch.empty(n, dtype=torch.int32, device=dev)
+        self._check(lib().cbaa_debug_map(self._h, _dptr(iip, "iip"), _dptr(oip, "oip"), n, C.c_void_p(cs.data_ptr()),
+                                         C.c_void_p(cols.data_ptr()), C.c_void_p(row.data_ptr()), _stream(stream)),
+                    "cbaa_debug_map")
+        return cs, cols.view(n, narr), row
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().cbaa_kernel_launches(self._h)
+
+    @property
+    def update_passes(self) -> int:
+        return lib().cbaa_update_passes(self._h)
+
+
+def _wrap_device(ptr: int, nbytes: int, device: int, owner):
+    """Zero-copy torch.uint8 view of library-owned device memory (via __cuda_array_interface__)."""
+    import torch
+
+    class _Mem:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                    "strides": None, "stream": None}
+
+    t = torch.as_tensor(_Mem(), device=f"cuda:{device}")
+    t._cbaa_owner = owner   # keep the handle alive while the view lives
+    return t

@@ -1,0 +1,682 @@
+// libcbaa.so — host side of the C ABI declared in include/cbaa.h.
+// Validation, handle/scratch ownership, launch configuration, the double-buffered
+// host-ingest pipeline, and result ordering.  All per-pair, per-column and per-tuple
+// work runs in the sm_100a kernels of kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "cbaa.h"
+#include "geometry.cuh"
+#include "kernels.cuh"
+
+using namespace cbaa;
+
+struct cbaa_handle {
+  cbaa_config cfg;
+  Geo G;
+  int device = 0;
+  int sms = 148;
+  int l2_bytes = 0;
+  uint32_t passes = 1;
+  uint32_t* cube = nullptr;
+  uint64_t cube_bytes = 0;
+  uint64_t cube_words = 0;
+  // detect scratch (one allocation, see alloc_scratch)
+  void* scratch = nullptr;
+  DetectScratch D{};
+  unsigned long long* skipped = nullptr;
+  size_t hdr_bytes = 0;   // bytes of the per-detect zeroed header (ztot, done, done_all, n_hits, n_cand)
+  // pinned host staging
+  cbaa_cs_stats* h_rec = nullptr;
+  unsigned long long* h_cnt = nullptr;
+  cbaa_host* h_hits = nullptr;
+  uint64_t h_hits_cap = 0;
+  // candidate recording (debug)
+  int record = 0;
+  // host-ingest pipeline
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  uint32_t* stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t stage_pairs = 0;
+  uint64_t launches = 0;
+  int upd_blocks = 0;
+  std::string err;
+};
+
+namespace {
+
+const char* g_codes[] = {"ok", "invalid config", "invalid argument", "CUDA error", "cube mismatch",
+                         "output capacity exceeded", "tuple cap exceeded", "out of device memory"};
+
+int fail(cbaa_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_fail(cbaa_handle* h, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (h) h->err = m;
+  return e == cudaErrorMemoryAllocation ? CBAA_E_NOMEM : CBAA_E_CUDA;
+}
+
+#define CK(h, call)                                      \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+// EP/CP lengths: |EP(i)| = CL_bs((i+1) mod |RA|) − CL_bs(i) mod L (Q6); |CP(i)| = cbn(i) − |EP(i)|.
+void ep_cp(const cbaa_config& c, int* ep, int* cp) {
+  int L = 32 - (int)c.r;
+  for (uint32_t i = 0; i < c.num_ra; ++i) {
+    int e = ((int)c.clbs[(i + 1) % c.num_ra] - (int)c.clbs[i]) % L;
+    if (e < 0) e += L;
+    ep[i] = e;
+    cp[i] = (int)c.cbn[i] - e;
+  }
+}
+
+int validate(const cbaa_config* c, std::string* why) {
+  auto bad = [&](const char* m) {
+    if (why) *why = m;
+    return CBAA_E_CONFIG;
+  };
+  if (!c) return bad("config is null");
+  if (c->r > 16) return bad("r must be <= 16");
+  if (c->num_ra < 2 || c->num_ra > CBAA_MAX_RA) return bad("num_ra must be in [2, 8] (a single RA cannot restore LP, S:66)");
+  if (c->num_va > CBAA_MAX_VA) return bad("num_va must be <= 8");
+  if (!pow2(c->g) || c->g < 32) return bad("g must be a power of two >= 32 (S:40, Q28)");
+  if (!(c->mangle_a & 1u)) return bad("mangle_a must be odd (S:40)");
+  int L = 32 - (int)c->r;
+  for (uint32_t i = 0; i < c->num_ra + c->num_va; ++i)
+    if (c->cbn[i] < 1 || (int)c->cbn[i] > L || c->cbn[i] > 24) return bad("cbn(i) must be in [1, min(L, 24)]");
+  for (uint32_t i = 0; i < c->num_ra; ++i) {
+    if ((int)c->clbs[i] >= L) return bad("clbs(i) must be < L = 32 - r (Q6)");
+    if (i && c->clbs[i] <= c->clbs[i - 1]) return bad("clbs must be strictly increasing (S:41)");
+  }
+  int ep[CBAA_MAX_RA], cp[CBAA_MAX_RA], sum = 0;
+  ep_cp(*c, ep, cp);
+  for (uint32_t i = 0; i < c->num_ra; ++i) sum += ep[i];
+  if (sum != L) return bad("sum of ep(i) must equal L = 32 - r (S:38)");
+  for (uint32_t i = 0; i < c->num_ra; ++i) {
+    if (cp[i] < 0) return bad("cp(i) = cbn(i) - ep(i) must be >= 0 (S:39)");
+    if (cp[i] > ep[(i + 1) % c->num_ra]) return bad("cp(i) must be <= ep((i+1) mod num_ra) (S:39)");
+  }
+  if (c->theta_formula != CBAA_THETA_PAPER && c->theta_formula != CBAA_THETA_INVERTED)
+    return bad("theta_formula must be CBAA_THETA_PAPER or CBAA_THETA_INVERTED");
+  if (c->direction != CBAA_DIR_NORMALIZED && c->direction != CBAA_DIR_INNER_PREFIX)
+    return bad("direction must be CBAA_DIR_NORMALIZED or CBAA_DIR_INNER_PREFIX");
+  if (c->n_prefixes > CBAA_MAX_PREFIXES) return bad("at most 16 inner prefixes");
+  uint64_t csb = 0;
+  for (uint32_t a = 0; a < c->num_ra + c->num_va; ++a) csb += ((uint64_t)1 << c->cbn[a]) * c->g;
+  if ((csb << c->r) / 8 > (16ull << 30) - 16) return bad("cube must be smaller than 16 GiB");
+  return CBAA_OK;
+}
+
+uint32_t inv_mod32(uint32_t a) {   // Newton iteration for the inverse of odd a modulo 2^32
+  uint32_t x = a;
+  for (int k = 0; k < 5; ++k) x *= 2u - a * x;
+  return x;
+}
+
+Geo derive(const cbaa_config& c) {
+  Geo G;
+  std::memset(&G, 0, sizeof G);
+  G.r = c.r;
+  G.L = 32 - c.r;
+  G.num_ra = c.num_ra;
+  G.num_va = c.num_va;
+  G.narr = c.num_ra + c.num_va;
+  G.g = c.g;
+  G.wpc = c.g / 32;
+  while ((1u << G.wpc_log2) < G.wpc) ++G.wpc_log2;
+  G.n_cs = 1u << c.r;
+  G.rmask = G.n_cs - 1u;
+  uint32_t off = 0;
+  for (uint32_t a = 0; a < G.narr; ++a) {
+    G.arr_off[a] = off;
+    G.cbn[a] = c.cbn[a];
+    G.ncols[a] = 1u << c.cbn[a];
+    G.colmask[a] = G.ncols[a] - 1u;
+    off += G.ncols[a] * G.wpc;
+  }
+  G.cs_words = off;
+  int ep[CBAA_MAX_RA], cp[CBAA_MAX_RA];
+  ep_cp(c, ep, cp);
+  uint32_t raoff = 0;
+  for (uint32_t i = 0; i < c.num_ra; ++i) {
+    G.clbs[i] = c.clbs[i];
+    G.ep[i] = (uint32_t)ep[i];
+    G.cp[i] = (uint32_t)cp[i];
+    G.sh[i] = 2 * G.L - c.clbs[i] - c.cbn[i];
+    G.ra_off[i] = raoff;
+    raoff += G.ncols[i];
+  }
+  G.ra_cols = raoff;
+  G.mangle_a = c.mangle_a;
+  G.mangle_b = c.mangle_b;
+  G.inv_a = inv_mod32(c.mangle_a);
+  G.bv_seed = c.bv_seed;
+  for (uint32_t j = 0; j < c.num_va; ++j) G.va_seeds[j] = c.va_seeds[j];
+  G.direction = c.direction;
+  G.theta_formula = c.theta_formula;
+  G.n_prefix = c.n_prefixes;
+  for (uint32_t k = 0; k < c.n_prefixes; ++k) {
+    G.prefix[k] = c.inner_prefix[k] & c.inner_mask[k];
+    G.pmask[k] = c.inner_mask[k];
+  }
+  G.tuple_cap = c.tuple_cap;
+  return G;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int alloc_scratch(cbaa_handle* h) {
+  const Geo& G = h->G;
+  const size_t n_cs = G.n_cs;
+  const uint32_t hit_cap = h->cfg.hit_capacity ? h->cfg.hit_capacity : (1u << 20);
+  // header: ztot[n_cs] done[n_cs] done_all n_hits n_cand skipped — zeroed per detect (skipped per reset)
+  size_t off = 0;
+  size_t o_ztot = off;
+  off += n_cs * 8;
+  size_t o_done = off;
+  off += align_up(n_cs * 4, 8);
+  size_t o_done_all = off;
+  off += 8;
+  size_t o_nhits = off;
+  off += 8;
+  size_t o_ncand = off;
+  off += 8;
+  h->hdr_bytes = off;
+  size_t o_skipped = off;
+  off += 8;
+  off = align_up(off, 256);
+  size_t o_rec = off;
+  off += align_up(n_cs * sizeof(cbaa_cs_stats), 256);
+  size_t o_prefix = off;
+  off += align_up((n_cs + 1) * 8, 256);
+  size_t o_zc = off;
+  off += align_up(n_cs * G.ra_cols * 4, 256);
+  size_t o_hc = off;
+  off += align_up(n_cs * G.ra_cols * 4, 256);
+  size_t o_hits = off;
+  off += align_up((size_t)hit_cap * sizeof(cbaa_host), 256);
+  char* base = nullptr;
+  CK(h, cudaMalloc(&base, off));
+  CK(h, cudaMemset(base, 0, off));
+  h->scratch = base;
+  DetectScratch& D = h->D;
+  D.ztot = (unsigned long long*)(base + o_ztot);
+  D.done = (unsigned int*)(base + o_done);
+  D.done_all = (unsigned int*)(base + o_done_all);
+  D.n_hits = (unsigned long long*)(base + o_nhits);
+  D.n_cand = (unsigned long long*)(base + o_ncand);
+  h->skipped = (unsigned long long*)(base + o_skipped);
+  D.rec = (cbaa_cs_stats*)(base + o_rec);
+  D.prefix = (unsigned long long*)(base + o_prefix);
+  D.zc = (uint32_t*)(base + o_zc);
+  D.hc = (uint32_t*)(base + o_hc);
+  D.hits = (cbaa_host*)(base + o_hits);
+  D.hit_cap = hit_cap;
+  D.cand = nullptr;
+  D.cand_cap = 0;
+  CK(h, cudaMallocHost(&h->h_rec, n_cs * sizeof(cbaa_cs_stats) + 64));
+  CK(h, cudaMallocHost(&h->h_cnt, 64));
+  h->h_hits_cap = 4096;
+  CK(h, cudaMallocHost(&h->h_hits, h->h_hits_cap * sizeof(cbaa_host)));
+  return CBAA_OK;
+}
+
+int launch_check(cbaa_handle* h, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(h, e, what);
+  ++h->launches;
+  return CBAA_OK;
+}
+
+int grid_for(const cbaa_handle* h, uint64_t work_items, int per_sm) {
+  uint64_t want = (work_items + kThreads - 1) / kThreads;
+  uint64_t cap = (uint64_t)h->sms * per_sm;
+  return (int)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+// One pass of Alg. 1 over n device pairs, restricted to cube words [lo, lo+span).
+int launch_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t lo, uint32_t span,
+                  bool count_skips, cudaStream_t s) {
+  uint64_t head = 0;
+  uintptr_t as = (uintptr_t)src, ad = (uintptr_t)dst;
+  bool vec = (as % 4 == 0) && (as % 16 == ad % 16);
+  if (vec) head = std::min<uint64_t>(n, ((16 - as % 16) % 16) / 4);
+  uint64_t n4 = vec ? (n - head) / 4 : 0;
+  if (!vec) head = n;   // everything scalar
+  uint64_t scalar = head + (n - head - 4 * n4);
+  uint64_t items = std::max(n4, scalar);
+  int grid = grid_for(h, items, h->upd_blocks);
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  unsigned long long* sk = count_skips ? h->skipped : nullptr;
+  const Geo& G = h->G;
+  if (G.num_ra == 3 && G.num_va == 1) {
+    if (prefix) k_update<3, 1, true><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+    else k_update<3, 1, false><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+  } else {
+    if (prefix) k_update<0, 0, true><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+    else k_update<0, 0, false><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+  }
+  return launch_check(h, "k_update");
+}
+
+int update_all_passes(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
+  const uint64_t W = h->cube_words;
+  for (uint32_t p = 0; p < h->passes; ++p) {
+    uint64_t lo = W * p / h->passes, hi = W * (p + 1) / h->passes;
+    int rc = launch_update(h, src, dst, n, (uint32_t)lo, (uint32_t)(hi - lo), p == 0, s);
+    if (rc) return rc;
+  }
+  return CBAA_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* cbaa_strerror(int code) {
+  int k = -code;
+  if (k < 0 || k >= (int)(sizeof g_codes / sizeof g_codes[0])) return "unknown error";
+  return g_codes[k];
+}
+
+const char* cbaa_last_error(const cbaa_handle* h) { return h ? h->err.c_str() : ""; }
+
+int cbaa_config_default(cbaa_config* out) {
+  if (!out) return CBAA_E_ARG;
+  std::memset(out, 0, sizeof *out);
+  out->r = 4;
+  out->num_ra = 3;
+  out->num_va = 1;
+  out->g = 4096;
+  for (int a = 0; a < 4; ++a) out->cbn[a] = 12;   // c(i) = 2^12 (Q9)
+  out->clbs[0] = 0;      // Q8
+  out->clbs[1] = 10;
+  out->clbs[2] = 20;
+  out->mangle_a = 0x9E3779B1u;   // Q3
+  out->mangle_b = 0x7F4A7C15u;
+  out->bv_seed = 0x85EBCA6Bu;    // Q4
+  out->va_seeds[0] = 0xC2B2AE35u;
+  out->theta_formula = CBAA_THETA_PAPER;
+  out->direction = CBAA_DIR_NORMALIZED;
+  out->tuple_cap = 1ull << 24;
+  return CBAA_OK;
+}
+
+int cbaa_config_validate(const cbaa_config* cfg, char* err, uint64_t errlen) {
+  std::string why;
+  int rc = validate(cfg, &why);
+  if (err && errlen) {
+    std::snprintf(err, (size_t)errlen, "%s", rc ? why.c_str() : "");
+  }
+  return rc;
+}
+
+uint64_t cbaa_cube_bytes(const cbaa_config* cfg) {
+  if (validate(cfg, nullptr)) return 0;
+  uint64_t csb = 0;
+  for (uint32_t a = 0; a < cfg->num_ra + cfg->num_va; ++a) csb += ((uint64_t)1 << cfg->cbn[a]) * cfg->g;
+  return (csb << cfg->r) / 8;
+}
+
+int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
+  if (!out) return CBAA_E_ARG;
+  *out = nullptr;
+  std::string why;
+  if (validate(cfg, &why)) {
+    std::fprintf(stderr, "cbaa_create: %s\n", why.c_str());
+    return CBAA_E_CONFIG;
+  }
+  cbaa_handle* h = new (std::nothrow) cbaa_handle();
+  if (!h) return CBAA_E_NOMEM;
+  h->cfg = *cfg;
+  h->G = derive(*cfg);
+  h->device = device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    delete h;
+    return CBAA_E_ARG;
+  }
+  DeviceGuard dg(device);
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, device);
+  h->cube_bytes = cbaa_cube_bytes(cfg);
+  h->cube_words = h->cube_bytes / 4;
+  int rc = CBAA_OK;
+  cudaError_t e = cudaMalloc(&h->cube, h->cube_bytes);
+  if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMalloc(cube)");
+  if (!rc) {
+    e = cudaMemset(h->cube, 0, h->cube_bytes);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemset(cube)");
+  }
+  if (!rc) rc = alloc_scratch(h);
+  if (rc) {
+    std::fprintf(stderr, "cbaa_create: %s\n", h->err.c_str());
+    cbaa_destroy(h);
+    return rc;
+  }
+  // Update passes: the RED rate collapses ~3x once the cube spills L2 (profiles/r01_redbench.jsonl),
+  // so the cube is split into address ranges that each fit 70% of L2.
+  if (cfg->update_passes) {
+    h->passes = cfg->update_passes;
+  } else {
+    double budget = 0.70 * (h->l2_bytes > 0 ? h->l2_bytes : (96 << 20));
+    h->passes = (uint32_t)std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget));
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, false>, kThreads, 0);
+  h->upd_blocks = std::max(1, occ);
+  *out = h;
+  return CBAA_OK;
+}
+
+void cbaa_destroy(cbaa_handle* h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  if (h->cube) cudaFree(h->cube);
+  if (h->scratch) cudaFree(h->scratch);
+  if (h->D.cand) cudaFree(h->D.cand);
+  if (h->h_rec) cudaFreeHost(h->h_rec);
+  if (h->h_cnt) cudaFreeHost(h->h_cnt);
+  if (h->h_hits) cudaFreeHost(h->h_hits);
+  for (int b = 0; b < 2; ++b) {
+    for (int a = 0; a < 2; ++a)
+      if (h->stage[b][a]) cudaFree(h->stage[b][a]);
+    if (h->ev_copied[b]) cudaEventDestroy(h->ev_copied[b]);
+    if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
+  }
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  delete h;
+}
+
+int cbaa_get_config(const cbaa_handle* h, cbaa_config* out) {
+  if (!h || !out) return CBAA_E_ARG;
+  *out = h->cfg;
+  return CBAA_OK;
+}
+
+int cbaa_reset(cbaa_handle* h, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t n16 = h->cube_bytes / 16;
+  k_zero<<<grid_for(h, n16, 4), kThreads, 0, s>>>((uint4*)h->cube, n16);
+  int rc = launch_check(h, "k_zero");
+  if (rc) return rc;
+  CK(h, cudaMemsetAsync(h->skipped, 0, 8, s));
+  return CBAA_OK;
+}
+
+int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (n == 0) return CBAA_OK;
+  if (!src || !dst) return fail(h, CBAA_E_ARG, "cbaa_update: null src/dst");
+  if (((uintptr_t)src | (uintptr_t)dst) & 3) return fail(h, CBAA_E_ARG, "cbaa_update: src/dst must be 4-byte aligned");
+  DeviceGuard dg(h->device);
+  return update_all_passes(h, src, dst, n, (cudaStream_t)stream);
+}
+
+int cbaa_update_host(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (n == 0) return CBAA_OK;
+  if (!src || !dst) return fail(h, CBAA_E_ARG, "cbaa_update_host: null src/dst");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t chunk = 1ull << 23;   // 8 Mi pairs = 64 MiB per buffer pair
+  if (!h->copy_stream) {
+    CK(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(h, cudaEventCreateWithFlags(&h->ev_copied[b], cudaEventDisableTiming));
+      CK(h, cudaEventCreateWithFlags(&h->ev_free[b], cudaEventDisableTiming));
+      for (int a = 0; a < 2; ++a) CK(h, cudaMalloc(&h->stage[b][a], chunk * 4));
+    }
+    h->stage_pairs = chunk;
+  }
+  // the copy stream may not start before earlier work on `s` that still reads the staging buffers
+  for (int b = 0; b < 2; ++b) {
+    CK(h, cudaEventRecord(h->ev_free[b], s));
+  }
+  uint64_t k = 0;
+  for (uint64_t off = 0; off < n; off += h->stage_pairs, ++k) {
+    const int b = (int)(k & 1);
+    const uint64_t m = std::min(h->stage_pairs, n - off);
+    CK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_free[b], 0));
+    CK(h, cudaMemcpyAsync(h->stage[b][0], src + off, m * 4, cudaMemcpyHostToDevice, h->copy_stream));
+    CK(h, cudaMemcpyAsync(h->stage[b][1], dst + off, m * 4, cudaMemcpyHostToDevice, h->copy_stream));
+    CK(h, cudaEventRecord(h->ev_copied[b], h->copy_stream));
+    CK(h, cudaStreamWaitEvent(s, h->ev_copied[b], 0));
+    int rc = update_all_passes(h, h->stage[b][0], h->stage[b][1], m, s);
+    if (rc) return rc;
+    CK(h, cudaEventRecord(h->ev_free[b], s));
+  }
+  return CBAA_OK;
+}
+
+int cbaa_skipped(cbaa_handle* h, uint64_t* out, cbaa_stream stream) {
+  if (!h || !out) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaMemcpyAsync(h->h_cnt, h->skipped, 8, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  *out = h->h_cnt[0];
+  return CBAA_OK;
+}
+
+int cbaa_merge(cbaa_handle* h, const void* const* cubes, int k, uint64_t nbytes, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (k < 0 || k > CBAA_MAX_MERGE || (k && !cubes)) return fail(h, CBAA_E_ARG, "cbaa_merge: bad k/cubes");
+  if (nbytes != h->cube_bytes)
+    return fail(h, CBAA_E_MISMATCH, "cbaa_merge: cube size differs from this handle's geometry (S:103)");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t n16 = h->cube_bytes / 16;
+  for (int j0 = 0; j0 < k; j0 += 16) {
+    MergeSrcs S{};
+    S.k = std::min(16, k - j0);
+    for (int j = 0; j < S.k; ++j) {
+      if (!cubes[j0 + j] || ((uintptr_t)cubes[j0 + j] & 15))
+        return fail(h, CBAA_E_ARG, "cbaa_merge: null or non-16-byte-aligned cube pointer");
+      S.p[j] = (const uint4*)cubes[j0 + j];
+    }
+    k_or_merge<<<grid_for(h, n16, 4), kThreads, 0, s>>>((uint4*)h->cube, S, n16);
+    int rc = launch_check(h, "k_or_merge");
+    if (rc) return rc;
+  }
+  return CBAA_OK;
+}
+
+int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
+                     cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (cs_lo >= cs_hi || cs_hi > h->G.n_cs) return fail(h, CBAA_E_ARG, "cbaa_merge_slice: bad CS range");
+  if (k < 0 || k > CBAA_MAX_MERGE || (k && !slices)) return fail(h, CBAA_E_ARG, "cbaa_merge_slice: bad k/slices");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t cs_bytes = (uint64_t)h->G.cs_words * 4;
+  uint64_t n16 = cs_bytes * (cs_hi - cs_lo) / 16;
+  uint4* dst = (uint4*)((char*)h->cube + cs_bytes * cs_lo);
+  for (int j0 = 0; j0 < k; j0 += 16) {
+    MergeSrcs S{};
+    S.k = std::min(16, k - j0);
+    for (int j = 0; j < S.k; ++j) {
+      if (!slices[j0 + j] || ((uintptr_t)slices[j0 + j] & 15))
+        return fail(h, CBAA_E_ARG, "cbaa_merge_slice: null or non-16-byte-aligned slice pointer");
+      S.p[j] = (const uint4*)slices[j0 + j];
+    }
+    k_or_merge<<<grid_for(h, n16, 4), kThreads, 0, s>>>(dst, S, n16);
+    int rc = launch_check(h, "k_or_merge");
+    if (rc) return rc;
+  }
+  return CBAA_OK;
+}
+
+static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uint32_t theta, int finish,
+                           cudaStream_t s) {
+  const Geo& G = h->G;
+  uint32_t cmax = 0;
+  for (uint32_t i = 0; i < G.num_ra; ++i) cmax = std::max(cmax, G.ncols[i]);
+  // columns per CTA: 8 warps × 8 columns each, fewer if the arrays are small
+  uint32_t chunk = std::min<uint32_t>(64, cmax);
+  uint32_t n_chunks = (cmax + chunk - 1) / chunk;
+  uint64_t grid = (uint64_t)n_range * G.num_ra * n_chunks;
+  if (grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
+  k_zero_hot<<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta, finish);
+  return launch_check(h, "k_zero_hot");
+}
+
+int cbaa_zero_counts(cbaa_handle* h, uint32_t* out, cbaa_stream stream) {
+  if (!h || !out) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_zero_hot(h, 0, h->G.n_cs, 0, 0, s);
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(out, h->D.zc, (size_t)h->G.n_cs * h->G.ra_cols * 4, cudaMemcpyDeviceToDevice, s));
+  return CBAA_OK;
+}
+
+int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t cs_hi, cbaa_host* out, uint64_t cap,
+                      uint64_t* n_out, cbaa_cs_stats* stats, cbaa_stream stream) {
+  if (!h || !n_out) return CBAA_E_ARG;
+  if (cs_lo >= cs_hi || cs_hi > h->G.n_cs) return fail(h, CBAA_E_ARG, "cbaa_detect: bad CS range");
+  if (cap && !out) return fail(h, CBAA_E_ARG, "cbaa_detect: out is null");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t n_range = cs_hi - cs_lo;
+  DetectScratch& D = h->D;
+  // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
+  CK(h, cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, s));
+  CK(h, cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), s));
+  int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, s);
+  if (rc) return rc;
+  const int grid = h->sms * 4;
+  if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, s>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+  else k_tuples<0><<<grid, kThreads, 0, s>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+  rc = launch_check(h, "k_tuples");
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaMemcpyAsync(h->h_cnt, D.n_hits, 8, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  const uint64_t total = h->h_cnt[0];
+  const uint64_t got = std::min<uint64_t>(total, D.hit_cap);
+  if (got > h->h_hits_cap) {
+    cudaFreeHost(h->h_hits);
+    h->h_hits = nullptr;
+    h->h_hits_cap = std::max<uint64_t>(got, 2 * h->h_hits_cap);
+    CK(h, cudaMallocHost(&h->h_hits, h->h_hits_cap * sizeof(cbaa_host)));
+  }
+  if (got) {
+    CK(h, cudaMemcpyAsync(h->h_hits, D.hits, got * sizeof(cbaa_host), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+  }
+  // output order of S:418: estimate descending, then ip ascending
+  std::sort(h->h_hits, h->h_hits + got, [](const cbaa_host& a, const cbaa_host& b) {
+    if (a.estimate != b.estimate) return a.estimate > b.estimate;
+    return a.ip < b.ip;
+  });
+  const uint64_t ncopy = std::min<uint64_t>(got, cap);
+  if (ncopy) std::memcpy(out, h->h_hits, ncopy * sizeof(cbaa_host));
+  *n_out = total;
+  if (stats) std::memcpy(stats, h->h_rec, (size_t)n_range * sizeof(cbaa_cs_stats));
+  bool overflow = false;
+  for (uint32_t k = 0; k < n_range; ++k) overflow |= h->h_rec[k].overflow != 0;
+  if (total > D.hit_cap)
+    return fail(h, CBAA_E_CAPACITY, "device hit buffer too small: raise cbaa_config.hit_capacity");
+  if (total > cap) return fail(h, CBAA_E_CAPACITY, "more hosts than cap: *n_out holds the required count");
+  if (overflow) return fail(h, CBAA_E_TUPLE_CAP, "a CS exceeded tuple_cap and was skipped (see stats.overflow)");
+  return CBAA_OK;
+}
+
+int cbaa_detect(cbaa_handle* h, uint32_t theta, cbaa_host* out, uint64_t cap, uint64_t* n_out, cbaa_cs_stats* stats,
+                cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  return cbaa_detect_range(h, theta, 0, h->G.n_cs, out, cap, n_out, stats, stream);
+}
+
+int cbaa_cube_view(cbaa_handle* h, void** dev_ptr, uint64_t* nbytes) {
+  if (!h || !dev_ptr || !nbytes) return CBAA_E_ARG;
+  *dev_ptr = h->cube;
+  *nbytes = h->cube_bytes;
+  return CBAA_OK;
+}
+
+int cbaa_hot_columns(cbaa_handle* h, uint32_t* out, cbaa_stream stream) {
+  if (!h || !out) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaMemcpyAsync(out, h->D.hc, (size_t)h->G.n_cs * h->G.ra_cols * 4, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  return CBAA_OK;
+}
+
+int cbaa_set_record_candidates(cbaa_handle* h, int enable, uint64_t capacity) {
+  if (!h) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  if (h->D.cand) {
+    cudaFree(h->D.cand);
+    h->D.cand = nullptr;
+    h->D.cand_cap = 0;
+  }
+  h->record = enable ? 1 : 0;
+  if (enable) {
+    CK(h, cudaMalloc(&h->D.cand, std::max<uint64_t>(capacity, 1) * 8));
+    h->D.cand_cap = std::max<uint64_t>(capacity, 1);
+  }
+  return CBAA_OK;
+}
+
+int cbaa_candidates(cbaa_handle* h, uint64_t* out, uint64_t cap, uint64_t* n_out, cbaa_stream stream) {
+  if (!h || !n_out) return CBAA_E_ARG;
+  if (!h->record) return fail(h, CBAA_E_ARG, "candidate recording is off");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaMemcpyAsync(h->h_cnt, h->D.n_cand, 8, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  uint64_t total = h->h_cnt[0];
+  uint64_t m = std::min(std::min(total, cap), h->D.cand_cap);
+  if (m) CK(h, cudaMemcpy(out, h->D.cand, m * 8, cudaMemcpyDeviceToHost));
+  *n_out = total;
+  return total > h->D.cand_cap ? fail(h, CBAA_E_CAPACITY, "candidate buffer too small") : CBAA_OK;
+}
+
+int cbaa_debug_map(cbaa_handle* h, const uint32_t* iip, const uint32_t* oip, uint64_t n, uint32_t* cs, uint32_t* cols,
+                   uint32_t* row, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (n == 0) return CBAA_OK;
+  if (!iip || !oip || !cs || !cols || !row) return fail(h, CBAA_E_ARG, "cbaa_debug_map: null pointer");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_debug_map<<<grid_for(h, n, 8), kThreads, 0, s>>>(h->G, iip, oip, n, cs, cols, row);
+  return launch_check(h, "k_debug_map");
+}
+
+uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0; }
+
+uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }
+
+}  // extern "C"

@@ -1,0 +1,452 @@
+// sm_100a kernels of the CBAA window path (DESIGN.md §6 lists each with its roofline).
+//   k_update      Alg. 1: 128-bit streaming loads of SoA pairs, 4 REDs per pair
+//   k_zero        window reset
+//   k_or_merge    global OR merge (Q1)
+//   k_zero_hot    zero counts (Alg. 2 input) + per-CS η/ε/θ_bn
+//                 + ordered hot-column compaction (Alg. 2) + tuple-space prefix
+//   k_tuples      Alg. 3: CP-join over HC(0)×…×HC(|RA|−1), warp-cooperative
+//                 union-column AND/popcount, output with Thm. 2 estimate
+//   k_debug_map   Alg. 1 mapping only (test hook)
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "geometry.cuh"
+
+namespace cbaa {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------- primitives
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_stream4(const uint32_t* p) {
+  // input pairs are read exactly once: evict-first so they do not displace the cube in L2
+  return __ldcs(reinterpret_cast<const uint4*>(p));
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool is_inner(const Geo& G, uint32_t ip) {
+  bool in = false;
+  for (uint32_t k = 0; k < G.n_prefix; ++k) in |= (ip & G.pmask[k]) == G.prefix[k];
+  return in;
+}
+
+// a0 (Q25): returns false if the pair has zero or two inner endpoints.
+template <bool PREFIX>
+__device__ __forceinline__ bool normalize(const Geo& G, uint32_t& s, uint32_t& d) {
+  if (!PREFIX) return true;
+  bool si = is_inner(G, s), di = is_inner(G, d);
+  if (si == di) return false;
+  if (di) {
+    uint32_t t = s;
+    s = d;
+    d = t;
+  }
+  return true;
+}
+
+// Alg. 1 for one normalised pair: |RA|+|VA| REDs, restricted to cube words [lo, lo+span).
+template <int NRA, int NVA>
+__device__ __forceinline__ void set_pair_bits(const Geo& G, uint32_t iip, uint32_t oip, uint32_t* __restrict__ cube,
+                                              uint32_t lo, uint32_t span) {
+  const int nra = NRA ? NRA : (int)G.num_ra;
+  const int nva = NRA ? NVA : (int)G.num_va;
+  uint32_t mi = G.mangle_a * iip + G.mangle_b;        // mangle (Q3)
+  uint32_t mo = G.mangle_a * oip + G.mangle_b;        // oip mangled too (Q2)
+  uint32_t cs = mi & G.rmask;                          // RP selects the CS
+  uint32_t lp = mi >> G.r;                             // LP
+  uint32_t row = mix32(mo ^ G.bv_seed) & (G.g - 1);    // bvIdx = H_bv(oip)
+  uint32_t bit = 1u << (row & 31);
+  uint32_t base = cs * G.cs_words + (row >> 5);
+  uint64_t dbl = ((uint64_t)lp << G.L) | lp;           // LP twice: a rotate becomes one shift (Q6/Q7)
+#pragma unroll
+  for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i) {
+    if (i < nra) {
+      uint32_t col = (uint32_t)(dbl >> G.sh[i]) & G.colmask[i];   // CL(i)
+      uint32_t w = base + G.arr_off[i] + (col << G.wpc_log2);
+      if (w - lo < span) red_or(cube + w, bit);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < (NRA ? NVA : CBAA_MAX_VA); ++j) {
+    if (j < nva) {
+      uint32_t a = (uint32_t)nra + j;
+      uint32_t col = mix32(lp ^ G.va_seeds[j]) & G.colmask[a];     // CL(j) = H_j(LP)
+      uint32_t w = base + G.arr_off[a] + (col << G.wpc_log2);
+      if (w - lo < span) red_or(cube + w, bit);
+    }
+  }
+}
+
+// Persistent grid-stride update.  Pairs [0, head) and [head + 4·n4, n) go one per thread;
+// [head, head + 4·n4) is 16-B aligned in both arrays and goes four per thread per step.
+template <int NRA, int NVA, bool PREFIX>
+__global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
+                                                     const uint32_t* __restrict__ dst, uint64_t head, uint64_t n4,
+                                                     uint64_t n, uint32_t* __restrict__ cube, uint32_t lo,
+                                                     uint32_t span, unsigned long long* __restrict__ skipped) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t skip = 0;
+  const uint64_t tail0 = head + 4 * n4;
+  if (gid < head || gid < n - tail0) {
+    uint64_t k[2] = {gid, tail0 + gid};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if ((t == 0 && gid < head) || (t == 1 && k[1] < n)) {
+        uint32_t s = src[k[t]], d = dst[k[t]];
+        if (normalize<PREFIX>(G, s, d)) set_pair_bits<NRA, NVA>(G, s, d, cube, lo, span);
+        else ++skip;
+      }
+    }
+  }
+  const uint32_t* s4 = src + head;
+  const uint32_t* d4 = dst + head;
+  for (uint64_t i = gid; i < n4; i += stride) {
+    uint4 s = ld_stream4(s4 + 4 * i);
+    uint4 d = ld_stream4(d4 + 4 * i);
+    uint32_t ss[4] = {s.x, s.y, s.z, s.w};
+    uint32_t dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      if (normalize<PREFIX>(G, ss[p], dd[p])) set_pair_bits<NRA, NVA>(G, ss[p], dd[p], cube, lo, span);
+      else ++skip;
+    }
+  }
+  if (PREFIX && skipped) {
+    skip = warp_sum(skip);
+    if ((threadIdx.x & 31) == 0 && skip) atomicAdd(skipped, (unsigned long long)skip);
+  }
+}
+
+// ---------------------------------------------------------------- reset / merge
+__global__ void __launch_bounds__(kThreads) k_zero(uint4* __restrict__ p, uint64_t n16) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
+struct MergeSrcs {
+  const uint4* p[16];
+  int k;
+};
+
+// dst |= src[0] | … | src[k−1] over n16 16-byte words ("bits OR").
+__global__ void __launch_bounds__(kThreads) k_or_merge(uint4* __restrict__ dst, const __grid_constant__ MergeSrcs S,
+                                                       uint64_t n16) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    uint4 a = dst[i];
+    for (int j = 0; j < S.k; ++j) {
+      uint4 b = __ldcs(S.p[j] + i);
+      a.x |= b.x;
+      a.y |= b.y;
+      a.z |= b.z;
+      a.w |= b.w;
+    }
+    dst[i] = a;
+  }
+}
+
+// ---------------------------------------------------------------- window-end detect
+// Zero bits of one column (g rows = wpc words), summed by one warp.
+__device__ __forceinline__ uint32_t column_popc(const Geo& G, const uint32_t* __restrict__ col, int lane) {
+  uint32_t pop = 0;
+  if ((G.wpc & 127u) == 0) {
+    const uint4* c4 = reinterpret_cast<const uint4*>(col);
+    for (uint32_t w = lane; w < (G.wpc >> 2); w += 32) {
+      uint4 v = __ldcg(c4 + w);
+      pop += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
+  } else {
+    for (uint32_t w = lane; w < G.wpc; w += 32) pop += __popc(__ldcg(col + w));
+  }
+  return warp_sum(pop);
+}
+
+// Per-CS window math in fp64 (Q12, Thm. 1, θ_bn P:261 / Q15, Q16).
+__device__ void cs_math(const Geo& G, uint64_t ztot, uint32_t theta, cbaa_cs_stats* rec) {
+  const double g = (double)G.g;
+  const double bits0 = (double)G.ncols[0] * g;
+  double eta = ztot == 0 ? (double)INFINITY : -bits0 * log((double)ztot / bits0);
+  double eps = 1.0;
+  for (uint32_t i = 0; i < G.narr; ++i) eps *= 1.0 - exp(-eta / ((double)G.ncols[i] * g));
+  const double cap = 1.0 - 9.5367431640625e-07;   // 1 − 2^−20
+  if (eps > cap) eps = cap;
+  double tbn = G.theta_formula == CBAA_THETA_PAPER ? g * (1.0 + eps) * exp(-(double)theta / g) - g * eps
+                                                   : g * (1.0 - eps) * exp(-(double)theta / g);
+  if (tbn < 0.0) tbn = 0.0;
+  double f = floor(tbn);
+  uint32_t zmax = f < 0.0 ? 0u : (f > g ? G.g : (uint32_t)f);
+  rec->ztot = ztot;
+  rec->eta = eta;
+  rec->eps = eps;
+  rec->theta_bn = tbn;
+  rec->zmax = zmax;
+}
+
+struct DetectScratch {
+  uint32_t* zc;                 // [n_cs][ra_cols]
+  uint32_t* hc;                 // [n_cs][ra_cols], first n_hot[i] of each RA(i) block valid
+  cbaa_cs_stats* rec;           // [n_cs]
+  unsigned long long* ztot;     // [n_cs] accumulators
+  unsigned int* done;           // [n_cs] CTA arrival counters
+  unsigned int* done_all;       // [1]
+  unsigned long long* prefix;   // [n_range + 1] tuple-space prefix (0 for overflowed CSs)
+  unsigned long long* n_hits;   // [1]
+  cbaa_host* hits;              // [hit_cap]
+  uint32_t hit_cap;
+  unsigned long long* n_cand;   // [1]   candidate recording (debug)
+  unsigned long long* cand;     // [cand_cap]
+  uint64_t cand_cap;
+};
+
+// grid = n_range · num_ra · n_chunks CTAs; one warp per column; the last CTA of each CS finishes
+// that CS (math + ordered HC compaction); the last CS overall writes the tuple prefix.
+__global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+                                                       const __grid_constant__ DetectScratch D, uint32_t cs_lo,
+                                                       uint32_t n_range, uint32_t chunk, uint32_t n_chunks,
+                                                       uint32_t theta, int finish) {
+  __shared__ unsigned long long s_part[kWarps];
+  __shared__ uint32_t s_wcnt[kWarps];
+  __shared__ int s_last;
+  __shared__ uint32_t s_zmax;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t by = blockIdx.x / n_chunks;       // (cs, RA i) of this CTA
+  const uint32_t cs = cs_lo + by / G.num_ra;
+  const uint32_t i = by % G.num_ra;
+  const uint32_t c0 = (blockIdx.x % n_chunks) * chunk;
+  const uint32_t c1 = min(c0 + chunk, G.ncols[i]);
+  unsigned long long part = 0;
+  const uint32_t* arr = cube + (size_t)cs * G.cs_words + G.arr_off[i];
+  uint32_t* zc = D.zc + (size_t)cs * G.ra_cols + G.ra_off[i];
+  for (uint32_t col = c0 + warp; col < c1; col += kWarps) {
+    uint32_t pop = column_popc(G, arr + ((size_t)col << G.wpc_log2), lane);
+    uint32_t z = G.g - pop;
+    if (lane == 0) {
+      zc[col] = z;
+      part += z;
+    }
+  }
+  if (!finish) return;
+  if (lane == 0) s_part[warp] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sum = 0;
+    for (int w = 0; w < kWarps; ++w) sum += s_part[w];
+    if (i == 0 && sum) atomicAdd(D.ztot + cs, sum);
+    __threadfence();
+    unsigned int old = atomicAdd(D.done + cs, 1u);
+    s_last = old == n_chunks * G.num_ra - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last CTA of this CS: fp64 math, then Alg. 2 in ascending column order
+  __threadfence();
+  cbaa_cs_stats* rec = D.rec + cs;
+  if (threadIdx.x == 0) {
+    unsigned long long zt = __ldcg(D.ztot + cs);
+    cs_math(G, zt, theta, rec);
+    s_zmax = rec->zmax;
+  }
+  __syncthreads();
+  const uint32_t zmax = s_zmax;
+  const uint32_t* zcs = D.zc + (size_t)cs * G.ra_cols;
+  uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
+  unsigned long long prod = 1;
+  for (uint32_t a = 0; a < G.num_ra; ++a) {
+    uint32_t base = 0;
+    for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads) {
+      uint32_t col = t0 + threadIdx.x;
+      bool hot = col < G.ncols[a] && __ldcg(zcs + G.ra_off[a] + col) <= zmax;   // P:272, Q16
+      unsigned int b = __ballot_sync(0xffffffffu, hot);
+      if (lane == 0) s_wcnt[warp] = __popc(b);
+      __syncthreads();
+      uint32_t off = base, tot = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        uint32_t c = s_wcnt[w];
+        if (w < warp) off += c;
+        tot += c;
+      }
+      if (hot) hcs[G.ra_off[a] + off + __popc(b & ((1u << lane) - 1u))] = col;
+      base += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) rec->n_hot[a] = base;
+    prod = (base != 0 && prod > ~0ull / base) ? ~0ull : prod * base;   // saturating ∏|HC(i)|
+  }
+  if (threadIdx.x == 0) {
+    rec->tuples = prod;
+    rec->overflow = prod > G.tuple_cap ? 1 : 0;
+    __threadfence();
+    unsigned int old = atomicAdd(D.done_all, 1u);
+    s_last = old == n_range - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last CS overall: exclusive prefix of the (capped) tuple counts over the range
+  __threadfence();
+  const uint32_t per = (n_range + kThreads - 1) / kThreads;
+  const uint32_t b0 = min(threadIdx.x * per, n_range), b1 = min(b0 + per, n_range);
+  unsigned long long loc = 0;
+  for (uint32_t k = b0; k < b1; ++k) {
+    const cbaa_cs_stats* r = D.rec + cs_lo + k;
+    int ovf = __ldcg(&r->overflow);
+    loc += ovf ? 0ull : __ldcg(reinterpret_cast<const unsigned long long*>(&r->tuples));
+  }
+  __shared__ unsigned long long s_scan[kThreads];
+  s_scan[threadIdx.x] = loc;
+  __syncthreads();
+  for (int o = 1; o < kThreads; o <<= 1) {   // Hillis-Steele inclusive scan
+    unsigned long long v = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    s_scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned long long run = s_scan[threadIdx.x] - loc;
+  for (uint32_t k = b0; k < b1; ++k) {
+    D.prefix[k] = run;
+    const cbaa_cs_stats* r = D.rec + cs_lo + k;
+    run += __ldcg(&r->overflow) ? 0ull : __ldcg(reinterpret_cast<const unsigned long long*>(&r->tuples));
+  }
+  if (threadIdx.x == kThreads - 1) D.prefix[n_range] = s_scan[kThreads - 1];
+}
+
+// Alg. 3 over the whole tuple space of the range.  One lane per tuple for the CP check
+// and LP assembly; passing tuples are then checked one at a time by the
+// whole warp: AND of the |RA|+|VA| columns, popcount, Z ≤ zmax.
+template <int NRA>
+__global__ void __launch_bounds__(kThreads) k_tuples(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+                                                     const __grid_constant__ DetectScratch D, uint32_t cs_lo,
+                                                     uint32_t n_range, int record) {
+  const int lane = threadIdx.x & 31;
+  const int nra = NRA ? NRA : (int)G.num_ra;
+  const unsigned long long total = __ldcg(D.prefix + n_range);
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  const uint32_t Lmask = G.L == 32 ? 0xffffffffu : ((1u << G.L) - 1u);
+  for (uint64_t t0 = warp_id * 32; t0 < total; t0 += n_warps * 32) {
+    const uint64_t t = t0 + lane;
+    bool pass = false;
+    uint32_t cs_rel = 0, lp = 0;
+    uint32_t cols[NRA ? NRA : CBAA_MAX_RA];
+    if (t < total) {
+      // CS of tuple t: last k with prefix[k] ≤ t (binary search; empty CSs have equal prefixes)
+      uint32_t lo = 0, hi = n_range;
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(D.prefix + mid) <= t) lo = mid;
+        else hi = mid;
+      }
+      cs_rel = lo;
+      const uint32_t cs = cs_lo + cs_rel;
+      const cbaa_cs_stats* rec = D.rec + cs;
+      uint64_t u = t - __ldg(D.prefix + cs_rel);
+      const uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
+#pragma unroll
+      for (int i = (NRA ? NRA : CBAA_MAX_RA) - 1; i >= 0; --i) {   // mixed radix, last index fastest
+        if (i < nra) {
+          uint32_t nh = __ldg(&rec->n_hot[i]);
+          uint64_t q = u / nh;
+          cols[i] = __ldg(hcs + G.ra_off[i] + (uint32_t)(u - q * nh));
+          u = q;
+        }
+      }
+      pass = true;
+#pragma unroll
+      for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i) {
+        if (i < nra) {
+          const int nx = (i + 1 == nra) ? 0 : i + 1;
+          uint32_t low = cols[i] & ((1u << G.cp[i]) - 1u);                 // CP of hc_i
+          uint32_t top = cols[nx] >> (G.cbn[nx] - G.cp[i]);               // first |CP(i)| bits of hc_{i+1}
+          pass &= low == top;
+          // EP(i) = high |EP(i)| bits of hc_i, at LP offsets clbs(i).. (mod L), MSB-first
+          uint64_t x = (uint64_t)(cols[i] >> G.cp[i]) << (2 * G.L - G.clbs[i] - G.ep[i]);
+          lp |= (uint32_t)((x >> G.L) | x) & Lmask;
+        }
+      }
+    }
+    unsigned int m = __ballot_sync(0xffffffffu, pass);
+    while (m) {
+      const int srcl = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t c_rel = __shfl_sync(0xffffffffu, cs_rel, srcl);
+      const uint32_t c_lp = __shfl_sync(0xffffffffu, lp, srcl);
+      const uint32_t cs = cs_lo + c_rel;
+      const uint32_t* csb = cube + (size_t)cs * G.cs_words;
+      const uint32_t* colp[CBAA_MAX_ARRAYS];
+#pragma unroll
+      for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i) {
+        uint32_t c = __shfl_sync(0xffffffffu, i < nra ? cols[i] : 0u, srcl);
+        if (i < nra) colp[i] = csb + G.arr_off[i] + ((size_t)c << G.wpc_log2);
+      }
+      for (uint32_t j = 0; j < G.num_va; ++j) {
+        uint32_t a = nra + j;
+        uint32_t c = mix32(c_lp ^ G.va_seeds[j]) & G.colmask[a];            // H_j(LP)
+        colp[a] = csb + G.arr_off[a] + ((size_t)c << G.wpc_log2);
+      }
+      uint32_t pop = 0;
+      for (uint32_t w = lane; w < G.wpc; w += 32) {
+        uint32_t v = 0xffffffffu;
+        for (uint32_t a = 0; a < G.narr; ++a) v &= __ldcg(colp[a] + w);   // UCol AND
+        pop += __popc(v);
+      }
+      pop = warp_sum(pop);
+      if (lane == 0) {
+        cbaa_cs_stats* rec = D.rec + cs;
+        const uint32_t z = G.g - pop;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&rec->candidates), 1ull);
+        if (record) {
+          unsigned long long k = atomicAdd(D.n_cand, 1ull);
+          if (k < D.cand_cap) D.cand[k] = ((unsigned long long)cs << 32) | c_lp;
+        }
+        if (z <= rec->zmax) {   // reject iff zero bits > θ_bn (Q16)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&rec->hits), 1ull);
+          unsigned long long k = atomicAdd(D.n_hits, 1ull);
+          if (k < D.hit_cap) {
+            const double g = (double)G.g;
+            double est = z == 0 ? (double)INFINITY : -g * log((double)z / (g - g * rec->eps));   // Thm. 2
+            if (est < 0.0) est = 0.0;
+            cbaa_host h;
+            h.ip = G.inv_a * (((c_lp << G.r) | cs) - G.mangle_b);      // unmangle
+            h.cs = cs;
+            h.lp = c_lp;
+            h.z = z;
+            h.estimate = est;
+            D.hits[k] = h;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Alg. 1 mapping for the unit parity tests (no cube access).
+__global__ void k_debug_map(const __grid_constant__ Geo G, const uint32_t* __restrict__ iip,
+                            const uint32_t* __restrict__ oip, uint64_t n, uint32_t* __restrict__ cs_out,
+                            uint32_t* __restrict__ cols_out, uint32_t* __restrict__ row_out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    uint32_t mi = G.mangle_a * iip[k] + G.mangle_b;
+    uint32_t mo = G.mangle_a * oip[k] + G.mangle_b;
+    uint32_t lp = mi >> G.r;
+    uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+    cs_out[k] = mi & G.rmask;
+    row_out[k] = mix32(mo ^ G.bv_seed) & (G.g - 1);
+    for (uint32_t i = 0; i < G.num_ra; ++i) cols_out[k * G.narr + i] = (uint32_t)(dbl >> G.sh[i]) & G.colmask[i];
+    for (uint32_t j = 0; j < G.num_va; ++j)
+      cols_out[k * G.narr + G.num_ra + j] = mix32(lp ^ G.va_seeds[j]) & G.colmask[G.num_ra + j];
+  }
+}
+
+}  // namespace cbaa

@@ -1,0 +1,341 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
+
+Bars: cube bytes, zero counts, hot-column lists, candidate sets, tuple counts, zmax and
+the super-host list (ip, cs, lp, Z) are bit-exact; η, ε, θ_bn and estimates agree within 1e-12 relative.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1901_06207_b200 import workload as W
+from tests.geometries import random_params
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+
+
+def handle(p, **kw):
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
+    return Cbaa(config_from_dict(dict(p, **kw)), 0)
+
+
+def gpu_cube(cb):
+    torch.cuda.synchronize()
+    return cb.cube().cpu().numpy()
+
+
+def assert_stats_equal(gs, os_):
+    assert len(gs) == len(os_)
+    for cs, (a, b) in enumerate(zip(gs, os_)):
+        for k in ("ztot", "zmax", "n_hot", "tuples", "candidates", "hits", "overflow"):
+            assert a[k] == b[k], (cs, k, a[k], b[k])
+        for k in ("eta", "eps", "theta_bn"):
+            if np.isinf(b[k]) or b[k] == 0:
+                assert a[k] == b[k], (cs, k)
+            else:
+                assert abs(a[k] - b[k]) <= RTOL * abs(b[k]), (cs, k, a[k], b[k])
+
+
+def assert_hosts_equal(gh, oh):
+    assert len(gh) == len(oh)
+    assert [tuple(int(h[f]) for f in ("ip", "cs", "lp", "z")) for h in gh] == \
+           [tuple(int(h[f]) for f in ("ip", "cs", "lp", "z")) for h in oh]
+    for a, b in zip(gh["estimate"], oh["estimate"]):
+        if np.isinf(b):
+            assert np.isinf(a)
+        else:
+            assert abs(a - b) <= RTOL * max(abs(b), 1.0), (a, b)
+
+
+def full_check(p, src, dst, theta, **kw):
+    cb = handle(p, **kw)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    hosts, stats, rc = cb.detect(theta)
+    cube = gpu_cube(cb)
+    ref, _ = O.update(p, src, dst)
+    assert np.array_equal(cube, ref)
+    st, oh, ostats = O.detect(p, ref, theta)
+    assert (rc == 0) == (st == 0)
+    assert_stats_equal(stats, ostats)
+    assert_hosts_equal(hosts, oh)
+    return cb, ref, hosts, stats
+
+
+# ------------------------------------------------------------------ mapping
+def test_debug_map_matches_oracle(paper, golden):
+    src, dst = W.random_pairs(20000, 1)
+    for p in [paper] + [random_params(s) for s in range(4)]:
+        cb = handle(p)
+        cs, cols, row = cb.debug_map(dev(src), dev(dst))
+        cs, cols, row = cs.cpu().numpy(), cols.cpu().numpy(), row.cpu().numpy()
+        for k in range(0, src.size, 37):
+            ocs, ocols, orow = O.map_pair(p, int(src[k]), int(dst[k]))
+            assert (cs[k], list(cols[k]), row[k]) == (ocs, ocols, orow)
+    g = {k: v[0] for k, v in golden("single_pair.txt").items()}
+    cb = handle(paper)
+    cs, cols, row = cb.debug_map(dev([g["iip"][0]]), dev([g["oip"][0]]))
+    assert int(cs[0]) == g["cs"][0] and int(row[0]) == g["row"][0] and cols[0].tolist() == g["cols"]
+
+
+# ------------------------------------------------------------------ update
+def test_c1_window_paper_geometry(paper):
+    """BASELINE config 1: 1M pairs, 20 planted scanners of cardinality 2000, θ = 1024."""
+    w = W.generate(W.C1, 1)
+    cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024)
+    assert set(w.planted) <= set(hosts["ip"].tolist())
+    zc = cb.zero_counts().cpu().numpy()
+    assert np.array_equal(zc.view(np.uint32), O.zero_counts_ra(paper, ref))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_geometries(seed):
+    p = random_params(seed, max_cube_bytes=1 << 24)
+    spec = W.WindowSpec(n=200_000, n_hosts=3000, n_flows=30000, scanners=(300, 600, 900), victims=(500,))
+    w = W.generate(spec, 100 + seed)
+    full_check(p, w.src, w.dst, theta=max(8, p["g"] // 2))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 7, 31, 33, 1023])
+def test_small_and_ragged(paper, n):
+    src, dst = W.random_pairs(max(n, 1), 5 + n)
+    src, dst = src[:n], dst[:n]
+    cb = handle(paper)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("off_s, off_d", [(1, 1), (2, 2), (3, 3), (1, 2), (0, 3)])
+def test_misaligned_inputs(paper, off_s, off_d):
+    """Any 4-byte alignment: head/tail peeling and the scalar path (src/dst misaligned differently)."""
+    src, dst = W.random_pairs(10_000, 11)
+    big_s = dev(np.concatenate([np.zeros(4, np.uint32), src]))
+    big_d = dev(np.concatenate([np.zeros(4, np.uint32), dst]))
+    n = 9_000
+    s = big_s[off_s: off_s + n]
+    d = big_d[off_d: off_d + n]
+    hs = big_s.cpu().numpy().view(np.uint32)[off_s: off_s + n]
+    hd = big_d.cpu().numpy().view(np.uint32)[off_d: off_d + n]
+    cb = handle(paper)
+    cb.reset()
+    cb.update(s, d)
+    ref, _ = O.update(paper, hs, hd)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("passes", [1, 2, 3, 7])
+def test_update_passes(paper, passes):
+    """The address-range passes change only the schedule, never the cube."""
+    src, dst = W.random_pairs(300_000, 3)
+    cb = handle(paper, update_passes=passes)
+    assert cb.update_passes == passes
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+def test_hot_spot_and_duplicates(paper):
+    """Every pair identical (a single word hammered) and one host with 50K distinct peers."""
+    n = 200_000
+    cb = handle(paper)
+    cb.reset()
+    src = np.full(n, 0x0A000001, np.uint32)
+    dst = np.full(n, 0x08080808, np.uint32)
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src[:1], dst[:1])
+    assert np.array_equal(gpu_cube(cb), ref)
+    dst2 = np.arange(n, dtype=np.uint32) % 50_000 + 0x20000000
+    full_check(paper, src, dst2, 1024)
+
+
+def test_reset_and_accumulate(paper):
+    a_s, a_d = W.random_pairs(50_000, 1)
+    b_s, b_d = W.random_pairs(50_000, 2)
+    cb = handle(paper)
+    cb.reset()
+    cb.update(dev(a_s), dev(a_d))
+    cb.update(dev(b_s), dev(b_d))
+    ref, _ = O.update(paper, np.concatenate([a_s, b_s]), np.concatenate([a_d, b_d]))
+    assert np.array_equal(gpu_cube(cb), ref)
+    cb.reset()
+    assert not gpu_cube(cb).any()
+
+
+def test_inner_prefix_direction(paper):
+    """a0: raw on-wire pairs with the prefix classifier == normalised pairs; 0/2-inner pairs skipped."""
+    spec = W.WindowSpec(n=300_000, n_hosts=5000, n_flows=40000, victims=(3000,), scanners=(2500,))
+    w = W.generate(spec, 4)
+    q = dict(paper, direction=1, prefixes=w.prefixes)
+    junk_s, junk_d = W.random_pairs(1000, 9)
+    inner = np.uint32(w.prefixes[0][0]) | np.arange(1000, dtype=np.uint32)
+    raw_s = np.concatenate([w.raw_src, junk_s, inner])
+    raw_d = np.concatenate([w.raw_dst, junk_d, inner[::-1]])
+    cb = handle(q)
+    cb.reset()
+    cb.update(dev(raw_s), dev(raw_d))
+    ref, skipped = O.update(q, raw_s, raw_d)
+    assert np.array_equal(gpu_cube(cb), ref)
+    assert cb.skipped() == skipped >= 1000
+    norm, _ = O.update(paper, w.src, w.dst)
+    nz = np.nonzero(norm)[0]
+    assert np.array_equal(np.bitwise_and(ref, norm)[nz], norm[nz])
+
+
+# ------------------------------------------------------------------ detect
+def test_detect_structures_c1(paper):
+    """Hot-column lists (Alg. 2) and the CP-join candidate set (Alg. 3) equal the oracle's."""
+    w = W.generate(W.C1, 2)
+    cb = handle(paper)
+    cb.record_candidates(True)
+    cb.reset()
+    cb.update(dev(w.src), dev(w.dst))
+    hosts, stats, rc = cb.detect(1024)
+    hc = cb.hot_columns()
+    ref, _ = O.update(paper, w.src, w.dst)
+    st, oh, ostats = O.detect(paper, ref, 1024)
+    assert_stats_equal(stats, ostats)
+    assert_hosts_equal(hosts, oh)
+    zc = O.zero_counts_ra(paper, ref)
+    c = 4096
+    cand = cb.candidates()
+    for cs in range(16):
+        for i in range(3):
+            blk = zc[(cs * 3 + i) * c: (cs * 3 + i + 1) * c]
+            want = np.nonzero(blk <= ostats[cs]["zmax"])[0]
+            got = hc[(cs * 3 + i) * c: (cs * 3 + i) * c + stats[cs]["n_hot"][i]]
+            assert np.array_equal(got, want)
+        ocand = O.candidates(paper, ref, cs, ostats[cs]["zmax"])
+        gcand = np.sort((cand[(cand >> np.uint64(32)) == cs] & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+        assert np.array_equal(gcand, np.sort(ocand))
+
+
+@pytest.mark.parametrize("theta", [256, 512, 2048, 4096, 8192])
+def test_thresholds(paper, theta):
+    spec = W.WindowSpec(n=600_000, n_hosts=20000, n_flows=150000, scanners=(300, 700, 1500, 3000, 6000, 12000))
+    w = W.generate(spec, 3)
+    full_check(paper, w.src, w.dst, theta)
+
+
+def test_inverted_theta_formula(paper):
+    w = W.generate(W.C1, 5)
+    full_check(dict(paper, theta_formula=1), w.src, w.dst, 1024)
+
+
+def test_tuple_cap_and_capacity(paper):
+    spec = W.WindowSpec(n=200_000, n_hosts=3000, n_flows=40000, scanners=(3000, 2500, 4000, 5000))
+    w = W.generate(spec, 6)
+    p = dict(paper, tuple_cap=0)
+    cb = handle(p)
+    cb.reset()
+    cb.update(dev(w.src), dev(w.dst))
+    from paper_1901_06207_b200.cbaa import E_TUPLE_CAP
+    hosts, stats, rc = cb.detect(1024)
+    ref, _ = O.update(p, w.src, w.dst)
+    st, oh, ostats = O.detect(p, ref, 1024)
+    assert rc == E_TUPLE_CAP and st == 1
+    assert_stats_equal(stats, ostats)
+    assert_hosts_equal(hosts, oh)
+    # capacity: ask for fewer hosts than exist
+    cb2 = handle(paper)
+    cb2.reset()
+    cb2.update(dev(w.src), dev(w.dst))
+    from paper_1901_06207_b200.cbaa import CbaaError, E_CAPACITY
+    with pytest.raises(CbaaError) as ei:
+        cb2.detect(1024, cap=2)
+    assert ei.value.code == E_CAPACITY
+
+
+def test_detect_range_matches_full(paper):
+    w = W.generate(W.C1, 3)
+    cb = handle(paper)
+    cb.reset()
+    cb.update(dev(w.src), dev(w.dst))
+    full, fstats, _ = cb.detect(1024)
+    parts, pstats = [], []
+    for lo, hi in ((0, 5), (5, 6), (6, 16)):
+        h, s, _ = cb.detect(1024, cs_lo=lo, cs_hi=hi)
+        parts.append(h)
+        pstats += s
+    merged = np.concatenate(parts)
+    merged = merged[np.lexsort((merged["ip"], -merged["estimate"]))]
+    assert np.array_equal(merged, full)
+    assert pstats == fstats
+
+
+def test_empty_window(paper):
+    cb = handle(paper)
+    cb.reset()
+    hosts, stats, rc = cb.detect(1024)
+    assert rc == 0 and hosts.size == 0
+    assert all(s["eta"] == 0.0 and s["eps"] == 0.0 and s["n_hot"] == [0, 0, 0] for s in stats)
+
+
+# ------------------------------------------------------------------ merge / routers
+@pytest.mark.parametrize("policy", ["hash-by-pair", "hash-by-inner", "round-robin"])
+def test_router_merge(paper, policy):
+    """Config 3 in miniature: k simulated routers (handles) OR-merged == the oracle of the whole stream."""
+    w = W.generate(W.WindowSpec(n=800_000, n_hosts=20000, n_flows=100000, scanners=(2000,) * 5), 9)
+    k = 4
+    part = W.partition(w.src.size, k, policy, w.src, w.dst)
+    routers = []
+    for rr in range(k):
+        sel = part == rr
+        h = handle(paper)
+        h.reset()
+        h.update(dev(w.src[sel]), dev(w.dst[sel]))
+        routers.append(h)
+    g = handle(paper)
+    g.reset()
+    g.merge(routers)
+    hosts, stats, rc = g.detect(1024)
+    ref, _ = O.update(paper, w.src, w.dst)
+    assert np.array_equal(gpu_cube(g), ref)
+    st, oh, ostats = O.detect(paper, ref, 1024)
+    assert_hosts_equal(hosts, oh)
+    # slice merge of CS range [4, 12) only
+    s = handle(paper)
+    s.reset()
+    cs_bytes = s.nbytes // 16
+    s.merge_slice([r.cube()[4 * cs_bytes: 12 * cs_bytes] for r in routers], 4, 12)
+    cube = gpu_cube(s)
+    assert np.array_equal(cube[4 * cs_bytes: 12 * cs_bytes], ref[4 * cs_bytes: 12 * cs_bytes])
+    assert not cube[: 4 * cs_bytes].any() and not cube[12 * cs_bytes:].any()
+
+
+def test_update_host_pipeline(paper):
+    """cbaa_update_host (pinned and pageable host arrays, > 1 staging chunk) == device update."""
+    src, dst = W.random_pairs(20_000_000, 13)
+    cb = handle(paper)
+    cb.reset()
+    ps = torch.from_numpy(src.view(np.int32)).pin_memory()
+    pd = torch.from_numpy(dst.view(np.int32)).pin_memory()
+    cb.update_host(ps, pd)
+    a = gpu_cube(cb)
+    cb.reset()
+    cb.update_host(src[:5_000_001], dst[:5_000_001])
+    cb.update_host(src[5_000_001:], dst[5_000_001:])
+    b = gpu_cube(cb)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    c = gpu_cube(cb)
+    assert np.array_equal(a, c) and np.array_equal(b, c)
+
+
+# ------------------------------------------------------------------ full size
+@pytest.mark.slow
+def test_c2_full_size(paper):
+    """BASELINE config 2 at full size (100M pairs, the bench workload and launch configuration):
+    whole-cube bytes and the complete detection against the oracle."""
+    w = W.generate(W.C2, 1, with_raw=False)
+    cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024)
+    assert cb.update_passes == 2
+    assert 550 <= len(hosts) <= 750
