@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""CBAA window benchmark (BASELINE.json metric: packet pairs/s per window update + window-end detect ms).
+
+One step = one window of the hot path: reset (a7) → update of the window's pairs (a0-a6) →
+[OR-merge over NVLink, a8, N > 1] → detect (a9-a14, host list filled).  Workload: BASELINE config 2
+(100M core-network-shaped pairs per GPU, Zipf hosts, ~0.1% super hosts, paper geometry, θ = 1024),
+synthetic and seeded.  Inputs (800 MB per GPU) exceed the 126 MB L2, so no extra flush.
+
+  python bench.py [--gpus N --steps K --warmup W]           # our CUDA path, one JSON line on rank 0
+  python bench.py --impl reference [...]                    # the CPU oracle as it stands (reference arm)
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; each rank is one edge router with its own
+100M-pair shard of one global window (weak scaling); max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packet pairs/sec per window update (1/2/4/8 B200) + window-end detect ms"
+THETA = 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["C2", "C1"], default="C2")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
+    ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(name, seed, rank, world):
+    from paper_1901_06207_b200 import workload as W
+    spec = W.C2 if name == "C2" else W.C1
+    # one global flow set (shared seed); each router sees its own packets of those flows
+    pseed = seed if world == 1 else seed * 1000 + rank + 1
+    return spec, W.generate(spec, seed, packet_seed=pseed, with_raw=False)
+
+
+def config_block(name, spec, world):
+    return {"workload": f"{name}: {spec.n // 1_000_000}M pairs/GPU, {spec.n_hosts} inner hosts, "
+                        f"{spec.n_flows / 1e6:.1f}M Zipf(s={spec.zipf_s}) flows, shuffled",
+            "pairs_per_gpu": spec.n, "global_pairs": spec.n * world,
+            "geometry": "r=4 |RA|=3 |VA|=1 g=4096 c=4096 (128 MiB cube, P:437)", "theta": THETA,
+            "parallelism": f"routers{world}" if world > 1 else "single",
+            "l2": "inputs 800 MB/GPU > 126 MB L2 (no extra flush); cube reset each window"}
+
+
+# --------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:   # no NVML: report it instead of guessing
+            self.N, self.err = None, str(e)
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
+                 k.startswith("nvmlClocksThrottleReason")}
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                mask = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if isinstance(bit, int) and bit and (mask & bit) == bit and "None" not in name and "All" not in name:
+                        self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.N:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.N:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.N:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def red_peak():
+    """Measured L2-resident random RED.OR rate (tools/redbench --quick), the update's roofline denominator."""
+    exe = os.path.join(ROOT, "tools", "redbench")
+    try:
+        out = subprocess.run([exe, "--quick"], capture_output=True, text=True, timeout=120).stdout
+        for line in out.splitlines():
+            d = json.loads(line)
+            if d.get("mode") == "red":
+                return d["Gops"] * 1e9
+    except Exception:
+        pass
+    return None
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_update_traffic.json")))
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    spec, w = workload(args.workload, args.seed, 0, 1)
+    p = O.default_params()
+    m = 1_000_000 if spec.n >= 1_000_000 else spec.n
+    times = []
+    for k in range(args.warmup + args.steps):
+        off = (k * m) % max(1, spec.n - m + 1)
+        t0 = time.perf_counter()
+        cube, _ = O.update(p, w.src[off:off + m], w.dst[off:off + m])
+        O.detect(p, cube, THETA)
+        t1 = time.perf_counter()
+        if k >= args.warmup:
+            times.append(t1 - t0)
+    tot = sum(times)
+    value = m * len(times) / tot
+    sample = f"{m} consecutive pairs of the {args.workload} window per step (update + detect, θ={THETA})"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config_block(args.workload, spec, 1),
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(w, seconds_budget=20.0):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same window."""
+    from oracle import oracle as O
+    p = O.default_params()
+    m = 10_000_000 if w.src.size >= 10_000_000 else w.src.size
+    t0 = time.perf_counter()
+    cube, _ = O.update(p, w.src[:m], w.dst[:m])
+    O.detect(p, cube, THETA)
+    t1 = time.perf_counter()
+    return {"value": m / (t1 - t0), "unit": "pairs/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {m} pairs of the window: oracle update + detect (θ={THETA}), {t1 - t0:.1f} s"}
+
+
+# --------------------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_06207_b200 import distributed as D
+    from paper_1901_06207_b200.cbaa import Cbaa, default_config
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    peak_red = red_peak() if rank == 0 else None
+    spec, w = workload(args.workload, args.seed, rank, world)
+    n = spec.n
+    src = torch.from_numpy(w.src.view(np.int32)).cuda()
+    dst = torch.from_numpy(w.dst.view(np.int32)).cuda()
+    cfg = default_config()
+    cfg.update_passes = args.passes
+    cfg.update_mode = 0 if args.update_mode == "test_set" else 1
+    cb = Cbaa(cfg, local)
+    n_cs = cb.n_cs
+    cs_bytes = cb.nbytes // n_cs
+    stream = torch.cuda.Stream()
+    cube_view = cb.cube()
+
+    def merge_slices(peers, lo, hi):
+        cb.merge_slice(peers, lo, hi, stream=stream)
+
+    def window(ev=None):
+        cb.reset(stream)
+        if ev:
+            ev[0].record(stream)
+        cb.update(src, dst, stream)
+        if ev:
+            ev[1].record(stream)
+        lo, hi = 0, n_cs
+        if world > 1:
+            with torch.cuda.stream(stream):
+                lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
+        hosts, stats, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream)
+        if ev:
+            ev[2].record(stream)
+        return D.gather_hosts(hosts, rank, world)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):   # at least 3 untimed warm-up windows
+            window()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = cb.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            hosts = window(evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = cb.kernel_launches - launches0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    post_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    # window-end detect latency alone: update finished, then detect until the host list is filled
+    det_ms = []
+    with torch.cuda.stream(stream):
+        for _ in range(10):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h, _, _ = cb.detect(THETA, stream=stream)
+            det_ms.append(1e3 * (time.perf_counter() - t0))
+
+    e2e = None
+    if not args.no_e2e:
+        ps = torch.from_numpy(w.src.view(np.int32)).pin_memory()
+        pd = torch.from_numpy(w.dst.view(np.int32)).pin_memory()
+        ke = min(args.steps, 5)
+        with torch.cuda.stream(stream):
+            cb.reset(stream)
+            cb.update_host(ps, pd, stream)
+            cb.detect(THETA, stream=stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nh = 0
+            a.record(stream)
+            for _ in range(ke):
+                cb.reset(stream)
+                cb.update_host(ps, pd, stream)     # pinned host → device inside the timed region
+                hh, st, _ = cb.detect(THETA, stream=stream)   # device → host of the result
+                nh = len(hh)
+            b.record(stream)
+            torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / ke
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 24 * nh + 104 * n_cs + 8,
+               "path": "cbaa_update_host (pinned, double-buffered chunks) + cbaa_detect"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    ms_step = elapsed_ms / args.steps
+    value = n * world * args.steps / (elapsed_ms / 1e3)
+    upd = statistics.median(upd_ms)
+    passes = cb.update_passes
+    algo_red = 4 * n
+    achieved_red = algo_red / (upd / 1e3)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    traffic = ncu_traffic()
+    roofline = {"kernel": "k_update (cbaa_update, all passes)", "bound": "l2_atomic",
+                "achieved": achieved_red / 1e9, "peak": (peak_red or float("nan")) / 1e9, "unit": "G RED/s",
+                "frac": achieved_red / peak_red if peak_red else None,
+                "traffic": (traffic or {}).get("dram_bytes_per_update"),
+                "algorithmic": f"4 single-bit RED.OR per pair (|RA|+|VA|) x {n} pairs per update, "
+                               f"{passes} address-range launches",
+                "peak_source": "tools/redbench --quick in this run: random red.global.or.b32 over a 64 MiB "
+                               "L2-resident buffer (not in MEASURED_PEAKS.json)",
+                "update_ms": upd, "launch_ms": upd / passes, "update_passes": passes,
+                "update_mode": args.update_mode}
+    roofline_hbm = {"bound": "hbm", "achieved": 8 * n / (upd / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": 8 * n / (upd / 1e3) / 1e9 / hbm,
+                    "note": "input stream, 8 B/pair algorithmic; peak = MEASURED_PEAKS.json hbm_gbs"}
+    line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config_block(args.workload, spec, world),
+            "detect_ms": statistics.median(det_ms), "update_ms": upd,
+            "post_update_ms": statistics.median(post_ms),
+            "update_pairs_per_s": n * world / (upd / 1e3),
+            "n_super_hosts": int(len(hosts)) if hosts is not None else None,
+            "roofline": roofline, "roofline_hbm": roofline_hbm,
+            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e,
+            "baseline_note": "paper publishes no pairs/s (BASELINE.md); its restore time is <11 ms on a Titan Xp"}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

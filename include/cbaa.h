@@ -57,6 +57,10 @@ extern "C" {
 #define CBAA_THETA_PAPER 0    /* θ_bn = g(1+ε)e^{−θ/g} − gε, P:261 (default)                     */
 #define CBAA_THETA_INVERTED 1 /* θ_bn = g(1−ε)e^{−θ/g}, Theorem 2 inverted (Q15)           */
 
+/* How the update kernel sets a bit; the resulting cube is identical (bits only go 0 -> 1). */
+#define CBAA_UPDATE_TEST_SET 0  /* L1-cached load of the word; RED.OR only if the bit is still 0 (default) */
+#define CBAA_UPDATE_RED 1       /* unconditional RED.OR per bit: the paper's write-only update   */
+
 #define CBAA_DIR_NORMALIZED 0   /* src = inner, dst = outer as given (Q25)                 */
 #define CBAA_DIR_INNER_PREFIX 1 /* classify by inner prefixes; swap or skip              */
 
@@ -85,7 +89,8 @@ typedef struct {
   uint32_t inner_mask[CBAA_MAX_PREFIXES]; /* ip is inner iff (ip & mask[k]) == prefix[k] for some k      */
   uint32_t update_passes;              /* address-range passes of the update (0 = auto)   */
   uint32_t hit_capacity;               /* device hit buffer entries per detect (0 = 2^20)               */
-  uint32_t reserved[6];
+  uint32_t update_mode;                /* CBAA_UPDATE_* (0 = CBAA_UPDATE_TEST_SET)         */
+  uint32_t reserved[5];
 } cbaa_config;
 
 /* One restored super host (Alg. 3 output). */

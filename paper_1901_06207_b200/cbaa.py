@@ -21,6 +21,7 @@ OK = 0
 E_CONFIG, E_ARG, E_CUDA, E_MISMATCH, E_CAPACITY, E_TUPLE_CAP, E_NOMEM = -1, -2, -3, -4, -5, -6, -7
 THETA_PAPER, THETA_INVERTED = 0, 1
 DIR_NORMALIZED, DIR_INNER_PREFIX = 0, 1
+UPDATE_TEST_SET, UPDATE_RED = 0, 1
 
 
 class Config(C.Structure):
@@ -33,7 +34,7 @@ class Config(C.Structure):
         ("theta_formula", C.c_int32), ("direction", C.c_int32), ("tuple_cap", C.c_uint64),
         ("n_prefixes", C.c_uint32), ("inner_prefix", C.c_uint32 * MAX_PREFIXES),
         ("inner_mask", C.c_uint32 * MAX_PREFIXES), ("update_passes", C.c_uint32), ("hit_capacity", C.c_uint32),
-        ("reserved", C.c_uint32 * 6),
+        ("update_mode", C.c_uint32), ("reserved", C.c_uint32 * 5),
     ]
 
     def to_dict(self) -> dict:
@@ -139,6 +140,7 @@ def config_from_dict(p: dict) -> Config:
         c.inner_prefix[k], c.inner_mask[k] = pre, mask
     c.update_passes = p.get("update_passes", 0)
     c.hit_capacity = p.get("hit_capacity", 0)
+    c.update_mode = p.get("update_mode", UPDATE_TEST_SET)
     return c
 
 

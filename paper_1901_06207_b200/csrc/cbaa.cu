@@ -127,6 +127,8 @@ int validate(const cbaa_config* c, std::string* why) {
   if (c->direction != CBAA_DIR_NORMALIZED && c->direction != CBAA_DIR_INNER_PREFIX)
     return bad("direction must be CBAA_DIR_NORMALIZED or CBAA_DIR_INNER_PREFIX");
   if (c->n_prefixes > CBAA_MAX_PREFIXES) return bad("at most 16 inner prefixes");
+  if (c->update_mode != CBAA_UPDATE_TEST_SET && c->update_mode != CBAA_UPDATE_RED)
+    return bad("update_mode must be CBAA_UPDATE_TEST_SET or CBAA_UPDATE_RED");
   uint64_t csb = 0;
   for (uint32_t a = 0; a < c->num_ra + c->num_va; ++a) csb += ((uint64_t)1 << c->cbn[a]) * c->g;
   if ((csb << c->r) / 8 > (16ull << 30) - 16) return bad("cube must be smaller than 16 GiB");
@@ -273,15 +275,30 @@ int launch_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   uint64_t items = std::max(n4, scalar);
   int grid = grid_for(h, items, h->upd_blocks);
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
   unsigned long long* sk = count_skips ? h->skipped : nullptr;
   const Geo& G = h->G;
-  if (G.num_ra == 3 && G.num_va == 1) {
-    if (prefix) k_update<3, 1, true><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
-    else k_update<3, 1, false><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+  const bool paper = G.num_ra == 3 && G.num_va == 1;
+#define CBAA_LAUNCH_UPD(NRA, NVA, MODE, PFX) \
+  k_update<NRA, NVA, MODE, PFX><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk)
+  if (paper) {
+    if (test) {
+      if (prefix) CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_TEST_SET, true);
+      else CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_TEST_SET, false);
+    } else {
+      if (prefix) CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_RED, true);
+      else CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_RED, false);
+    }
   } else {
-    if (prefix) k_update<0, 0, true><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
-    else k_update<0, 0, false><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk);
+    if (test) {
+      if (prefix) CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_TEST_SET, true);
+      else CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_TEST_SET, false);
+    } else {
+      if (prefix) CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_RED, true);
+      else CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_RED, false);
+    }
   }
+#undef CBAA_LAUNCH_UPD
   return launch_check(h, "k_update");
 }
 
@@ -390,7 +407,7 @@ int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
     h->passes = (uint32_t)std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget));
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, false>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
   h->upd_blocks = std::max(1, occ);
   *out = h;
   return CBAA_OK;

@@ -55,42 +55,96 @@ __device__ __forceinline__ bool normalize(const Geo& G, uint32_t& s, uint32_t& d
   return true;
 }
 
-// Alg. 1 for one normalised pair: |RA|+|VA| REDs, restricted to cube words [lo, lo+span).
+// Word index of every bit Alg. 1 sets for one normalised pair, and the bit mask.
+// Arrays: RA(0..nra−1) then VA(0..nva−1).  Words outside [lo, lo+span) become kNoWord.
+constexpr uint32_t kNoWord = 0xffffffffu;
+
 template <int NRA, int NVA>
-__device__ __forceinline__ void set_pair_bits(const Geo& G, uint32_t iip, uint32_t oip, uint32_t* __restrict__ cube,
-                                              uint32_t lo, uint32_t span) {
-  const int nra = NRA ? NRA : (int)G.num_ra;
-  const int nva = NRA ? NVA : (int)G.num_va;
+__device__ __forceinline__ uint32_t pair_targets(const Geo& G, uint32_t iip, uint32_t oip, uint32_t lo, uint32_t span,
+                                                 uint32_t* w) {
   uint32_t mi = G.mangle_a * iip + G.mangle_b;        // mangle (Q3)
   uint32_t mo = G.mangle_a * oip + G.mangle_b;        // oip mangled too (Q2)
   uint32_t cs = mi & G.rmask;                          // RP selects the CS
   uint32_t lp = mi >> G.r;                             // LP
   uint32_t row = mix32(mo ^ G.bv_seed) & (G.g - 1);    // bvIdx = H_bv(oip)
-  uint32_t bit = 1u << (row & 31);
   uint32_t base = cs * G.cs_words + (row >> 5);
   uint64_t dbl = ((uint64_t)lp << G.L) | lp;           // LP twice: a rotate becomes one shift (Q6/Q7)
 #pragma unroll
-  for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i) {
-    if (i < nra) {
-      uint32_t col = (uint32_t)(dbl >> G.sh[i]) & G.colmask[i];   // CL(i)
-      uint32_t w = base + G.arr_off[i] + (col << G.wpc_log2);
-      if (w - lo < span) red_or(cube + w, bit);
-    }
+  for (int i = 0; i < NRA; ++i) {
+    uint32_t col = (uint32_t)(dbl >> G.sh[i]) & G.colmask[i];     // CL(i)
+    uint32_t x = base + G.arr_off[i] + (col << G.wpc_log2);
+    w[i] = x - lo < span ? x : kNoWord;
   }
 #pragma unroll
-  for (int j = 0; j < (NRA ? NVA : CBAA_MAX_VA); ++j) {
-    if (j < nva) {
-      uint32_t a = (uint32_t)nra + j;
-      uint32_t col = mix32(lp ^ G.va_seeds[j]) & G.colmask[a];     // CL(j) = H_j(LP)
-      uint32_t w = base + G.arr_off[a] + (col << G.wpc_log2);
-      if (w - lo < span) red_or(cube + w, bit);
-    }
+  for (int j = 0; j < NVA; ++j) {
+    uint32_t col = mix32(lp ^ G.va_seeds[j]) & G.colmask[NRA + j];   // CL(j) = H_j(LP)
+    uint32_t x = base + G.arr_off[NRA + j] + (col << G.wpc_log2);
+    w[NRA + j] = x - lo < span ? x : kNoWord;
+  }
+  return 1u << (row & 31);
+}
+
+// Generic geometry (runtime |RA|, |VA|): one pair at a time.
+template <int MODE>
+__device__ __forceinline__ void set_pair_generic(const Geo& G, uint32_t iip, uint32_t oip, uint32_t* __restrict__ cube,
+                                                 uint32_t lo, uint32_t span) {
+  uint32_t mi = G.mangle_a * iip + G.mangle_b;
+  uint32_t mo = G.mangle_a * oip + G.mangle_b;
+  uint32_t cs = mi & G.rmask;
+  uint32_t lp = mi >> G.r;
+  uint32_t row = mix32(mo ^ G.bv_seed) & (G.g - 1);
+  uint32_t bit = 1u << (row & 31);
+  uint32_t base = cs * G.cs_words + (row >> 5);
+  uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+  for (uint32_t a = 0; a < G.narr; ++a) {
+    uint32_t col = a < G.num_ra ? (uint32_t)(dbl >> G.sh[a]) & G.colmask[a]
+                                : mix32(lp ^ G.va_seeds[a - G.num_ra]) & G.colmask[a];
+    uint32_t x = base + G.arr_off[a] + (col << G.wpc_log2);
+    if (x - lo >= span) continue;
+    if (MODE == CBAA_UPDATE_TEST_SET && (__ldca(cube + x) & bit)) continue;
+    red_or(cube + x, bit);
+  }
+}
+
+// Four pairs of the fixed paper-shaped geometry (NRA RAs + NVA VAs): all 4·(NRA+NVA) word indices
+// first, then (TEST_SET) all the L1-cached loads back to back, then the REDs still needed.
+// Skipping a RED whose bit is already 1 leaves the cube unchanged: bits only go 0 → 1 inside a
+// window and L1 is invalidated at every kernel boundary, so a stale 0 only costs a redundant RED.
+template <int NRA, int NVA, int MODE, bool PREFIX>
+__device__ __forceinline__ void set_quad(const Geo& G, uint32_t* ss, uint32_t* dd, uint32_t* __restrict__ cube,
+                                         uint32_t lo, uint32_t span, uint32_t& skip) {
+  constexpr int NA = NRA + NVA;
+  uint32_t w[4][NA], bit[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    bool ok = normalize<PREFIX>(G, ss[p], dd[p]);
+    skip += ok ? 0u : 1u;
+    bit[p] = pair_targets<NRA, NVA>(G, ss[p], dd[p], lo, ok ? span : 0u, w[p]);
+  }
+  if (MODE == CBAA_UPDATE_TEST_SET) {
+    uint32_t v[4][NA];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int a = 0; a < NA; ++a) v[p][a] = w[p][a] != kNoWord ? __ldca(cube + w[p][a]) : bit[p];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (!(v[p][a] & bit[p])) red_or(cube + w[p][a], bit[p]);
+  } else {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (w[p][a] != kNoWord) red_or(cube + w[p][a], bit[p]);
   }
 }
 
 // Persistent grid-stride update.  Pairs [0, head) and [head + 4·n4, n) go one per thread;
 // [head, head + 4·n4) is 16-B aligned in both arrays and goes four per thread per step.
-template <int NRA, int NVA, bool PREFIX>
+// NRA = 0 selects the generic (runtime-geometry) path.
+template <int NRA, int NVA, int MODE, bool PREFIX>
 __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
                                                      const uint32_t* __restrict__ dst, uint64_t head, uint64_t n4,
                                                      uint64_t n, uint32_t* __restrict__ cube, uint32_t lo,
@@ -105,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo
     for (int t = 0; t < 2; ++t) {
       if ((t == 0 && gid < head) || (t == 1 && k[1] < n)) {
         uint32_t s = src[k[t]], d = dst[k[t]];
-        if (normalize<PREFIX>(G, s, d)) set_pair_bits<NRA, NVA>(G, s, d, cube, lo, span);
+        if (normalize<PREFIX>(G, s, d)) set_pair_generic<MODE>(G, s, d, cube, lo, span);
         else ++skip;
       }
     }
@@ -117,10 +171,14 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo
     uint4 d = ld_stream4(d4 + 4 * i);
     uint32_t ss[4] = {s.x, s.y, s.z, s.w};
     uint32_t dd[4] = {d.x, d.y, d.z, d.w};
+    if (NRA) {
+      set_quad<(NRA ? NRA : 1), NVA, MODE, PREFIX>(G, ss, dd, cube, lo, span, skip);
+    } else {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      if (normalize<PREFIX>(G, ss[p], dd[p])) set_pair_bits<NRA, NVA>(G, ss[p], dd[p], cube, lo, span);
-      else ++skip;
+      for (int p = 0; p < 4; ++p) {
+        if (normalize<PREFIX>(G, ss[p], dd[p])) set_pair_generic<MODE>(G, ss[p], dd[p], cube, lo, span);
+        else ++skip;
+      }
     }
   }
   if (PREFIX && skipped) {

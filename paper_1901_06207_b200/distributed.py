@@ -1,0 +1,59 @@
+"""Multi-GPU window: the paper's distributed edge routers on one NVLink domain.
+
+Each rank is one local server: it updates its own packet shard into its own cube (no communication
+during the window).  At window end the global CBA is the bitwise OR of the local cubes (Q1).
+NCCL has no bitwise OR reduction, so the exchange is reduce-scatter shaped:
+
+  * rank p owns the CS range [lo_p, hi_p) (Alg. 2/3 are independent per CS);
+  * ``all_to_all_single`` sends every rank the bytes of its owned CSs from every peer cube;
+  * the owner ORs the k−1 received slices into its own slice (``cbaa_merge_slice`` kernel);
+  * the owner runs detect on its CSs only; the small host lists are gathered to rank 0.
+
+Per-GPU traffic is (k−1)/k of one cube each way instead of (k−1) cubes for an all-gather.
+The orchestration is backend-agnostic so that the gloo CPU tests can drive it with the oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def owned_range(rank: int, world: int, n_cs: int):
+    """Contiguous CS range of a rank (every CS owned by exactly one rank)."""
+    return rank * n_cs // world, (rank + 1) * n_cs // world
+
+
+def exchange_owned(cube, rank: int, world: int, n_cs: int, cs_bytes: int, merge_slices, group=None):
+    """OR-reduce-scatter of per-rank cubes by CS ownership.
+
+    cube:          this rank's cube as a contiguous uint8 torch tensor (device or CPU per backend)
+    merge_slices:  callable(list_of_peer_slices, lo, hi) that ORs the peers' bytes of CSs [lo, hi)
+                   into this rank's cube (the product passes Cbaa.merge_slice).
+    Returns the owned (lo, hi)."""
+    import torch
+    import torch.distributed as dist
+
+    lo, hi = owned_range(rank, world, n_cs)
+    if world == 1:
+        return lo, hi
+    in_splits = [(owned_range(k, world, n_cs)[1] - owned_range(k, world, n_cs)[0]) * cs_bytes for k in range(world)]
+    mine = (hi - lo) * cs_bytes
+    out = torch.empty(mine * world, dtype=torch.uint8, device=cube.device)
+    dist.all_to_all_single(out, cube, output_split_sizes=[mine] * world, input_split_sizes=in_splits, group=group)
+    peers = [out[k * mine:(k + 1) * mine] for k in range(world) if k != rank]
+    if mine:
+        merge_slices(peers, lo, hi)
+    return lo, hi
+
+
+def gather_hosts(hosts: np.ndarray, rank: int, world: int, group=None):
+    """Collect every rank's host list on rank 0, in the output order of S:418."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return hosts
+    objs = [None] * world if rank == 0 else None
+    dist.gather_object(hosts, objs, dst=0, group=group)
+    if rank != 0:
+        return None
+    allh = np.concatenate(objs) if objs else hosts[:0]
+    return allh[np.lexsort((allh["ip"], -allh["estimate"]))]

@@ -99,14 +99,15 @@ def test_random_geometries(seed):
     p = random_params(seed, max_cube_bytes=1 << 24)
     spec = W.WindowSpec(n=200_000, n_hosts=3000, n_flows=30000, scanners=(300, 600, 900), victims=(500,))
     w = W.generate(spec, 100 + seed)
-    full_check(p, w.src, w.dst, theta=max(8, p["g"] // 2))
+    full_check(p, w.src, w.dst, theta=max(8, p["g"] // 2), update_mode=seed % 2)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 7, 31, 33, 1023])
-def test_small_and_ragged(paper, n):
+def test_small_and_ragged(paper, n, mode):
     src, dst = W.random_pairs(max(n, 1), 5 + n)
     src, dst = src[:n], dst[:n]
-    cb = handle(paper)
+    cb = handle(paper, update_mode=mode)
     cb.reset()
     cb.update(dev(src), dev(dst))
     ref, _ = O.update(paper, src, dst)
@@ -131,11 +132,13 @@ def test_misaligned_inputs(paper, off_s, off_d):
     assert np.array_equal(gpu_cube(cb), ref)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("passes", [1, 2, 3, 7])
-def test_update_passes(paper, passes):
-    """The address-range passes change only the schedule, never the cube."""
+def test_update_passes(paper, passes, mode):
+    """The address-range passes and the update mode (test-and-set vs plain RED) change
+    only the schedule, never the cube."""
     src, dst = W.random_pairs(300_000, 3)
-    cb = handle(paper, update_passes=passes)
+    cb = handle(paper, update_passes=passes, update_mode=mode)
     assert cb.update_passes == passes
     cb.reset()
     cb.update(dev(src), dev(dst))
@@ -143,10 +146,11 @@ def test_update_passes(paper, passes):
     assert np.array_equal(gpu_cube(cb), ref)
 
 
-def test_hot_spot_and_duplicates(paper):
+@pytest.mark.parametrize("mode", [0, 1])
+def test_hot_spot_and_duplicates(paper, mode):
     """Every pair identical (a single word hammered) and one host with 50K distinct peers."""
     n = 200_000
-    cb = handle(paper)
+    cb = handle(paper, update_mode=mode)
     cb.reset()
     src = np.full(n, 0x0A000001, np.uint32)
     dst = np.full(n, 0x08080808, np.uint32)
@@ -154,7 +158,7 @@ def test_hot_spot_and_duplicates(paper):
     ref, _ = O.update(paper, src[:1], dst[:1])
     assert np.array_equal(gpu_cube(cb), ref)
     dst2 = np.arange(n, dtype=np.uint32) % 50_000 + 0x20000000
-    full_check(paper, src, dst2, 1024)
+    full_check(paper, src, dst2, 1024, update_mode=mode)
 
 
 def test_reset_and_accumulate(paper):
@@ -338,4 +342,7 @@ def test_c2_full_size(paper):
     w = W.generate(W.C2, 1, with_raw=False)
     cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024)
     assert cb.update_passes == 2
+    cb.reset()
+    cb.update_host(w.src, w.dst)                 # the e2e path of bench.py, same window
+    assert np.array_equal(gpu_cube(cb), ref)
     assert 550 <= len(hosts) <= 750
