@@ -255,7 +255,9 @@ class Cbaa:
                raise_on_overflow: bool = False):
         """Window end: returns (hosts structured array, per-CS stats list, status code)."""
         cs_hi = self.n_cs if cs_hi is None else cs_hi
-        out = np.zeros(max(cap, 1), dtype=HOST_DTYPE)
+        out = getattr(self, "_out", None)
+        if out is None or out.size < max(cap, 1):
+            out = self._out = np.empty(max(cap, 1), dtype=HOST_DTYPE)   # reused across windows
         stats = (CsStats * (cs_hi - cs_lo))()
         n = C.c_uint64()
         rc = lib().cbaa_detect_range(self._h, theta, cs_lo, cs_hi, out.ctypes.data_as(C.c_void_p), cap,

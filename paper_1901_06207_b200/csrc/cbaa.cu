@@ -32,11 +32,12 @@ struct cbaa_handle {
   void* scratch = nullptr;
   DetectScratch D{};
   unsigned long long* skipped = nullptr;
-  size_t hdr_bytes = 0;   // bytes of the per-detect zeroed header (ztot, done, done_all, n_hits, n_cand)
+  size_t hdr_bytes = 0;   // bytes of the per-detect zeroed header (ztot, done, done_all, n_cand)
   // pinned host staging
   cbaa_cs_stats* h_rec = nullptr;
   unsigned long long* h_cnt = nullptr;
-  cbaa_host* h_hits = nullptr;
+  void* h_res = nullptr;        // pinned mirror of the device result block
+  cbaa_host* h_hits = nullptr;  // = h_res + 64
   uint64_t h_hits_cap = 0;
   // candidate recording (debug)
   int record = 0;
@@ -197,15 +198,14 @@ int alloc_scratch(cbaa_handle* h) {
   const Geo& G = h->G;
   const size_t n_cs = G.n_cs;
   const uint32_t hit_cap = h->cfg.hit_capacity ? h->cfg.hit_capacity : (1u << 20);
-  // header: ztot[n_cs] done[n_cs] done_all n_hits n_cand skipped — zeroed per detect (skipped per reset)
+  // header: ztot[n_cs] done[n_cs] done_all n_cand skipped — zeroed per detect (skipped per reset);
+  // n_hits is zeroed by k_zero_hot
   size_t off = 0;
   size_t o_ztot = off;
   off += n_cs * 8;
   size_t o_done = off;
   off += align_up(n_cs * 4, 8);
   size_t o_done_all = off;
-  off += 8;
-  size_t o_nhits = off;
   off += 8;
   size_t o_ncand = off;
   off += 8;
@@ -221,8 +221,9 @@ int alloc_scratch(cbaa_handle* h) {
   off += align_up(n_cs * G.ra_cols * 4, 256);
   size_t o_hc = off;
   off += align_up(n_cs * G.ra_cols * 4, 256);
-  size_t o_hits = off;
-  off += align_up((size_t)hit_cap * sizeof(cbaa_host), 256);
+  size_t o_nhits = off;            // result block: [n_hits | pad to 64 B | hits ...], copied to the host in one go
+  size_t o_hits = off + 64;
+  off += 64 + align_up((size_t)hit_cap * sizeof(cbaa_host), 256);
   char* base = nullptr;
   CK(h, cudaMalloc(&base, off));
   CK(h, cudaMemset(base, 0, off));
@@ -245,7 +246,8 @@ int alloc_scratch(cbaa_handle* h) {
   CK(h, cudaMallocHost(&h->h_rec, n_cs * sizeof(cbaa_cs_stats) + 64));
   CK(h, cudaMallocHost(&h->h_cnt, 64));
   h->h_hits_cap = 4096;
-  CK(h, cudaMallocHost(&h->h_hits, h->h_hits_cap * sizeof(cbaa_host)));
+  CK(h, cudaMallocHost(&h->h_res, 64 + h->h_hits_cap * sizeof(cbaa_host)));
+  h->h_hits = (cbaa_host*)((char*)h->h_res + 64);
   return CBAA_OK;
 }
 
@@ -421,7 +423,7 @@ void cbaa_destroy(cbaa_handle* h) {
   if (h->D.cand) cudaFree(h->D.cand);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   if (h->h_cnt) cudaFreeHost(h->h_cnt);
-  if (h->h_hits) cudaFreeHost(h->h_hits);
+  if (h->h_res) cudaFreeHost(h->h_res);
   for (int b = 0; b < 2; ++b) {
     for (int a = 0; a < 2; ++a)
       if (h->stage[b][a]) cudaFree(h->stage[b][a]);
@@ -563,7 +565,12 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   uint32_t n_chunks = (cmax + chunk - 1) / chunk;
   uint64_t grid = (uint64_t)n_range * G.num_ra * n_chunks;
   if (grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
-  k_zero_hot<<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta, finish);
+  if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
+    k_zero_hot<true><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
+                                                         finish);
+  else
+    k_zero_hot<false><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
+                                                          finish);
   return launch_check(h, "k_zero_hot");
 }
 
@@ -596,19 +603,26 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   else k_tuples<0><<<grid, kThreads, 0, s>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
   rc = launch_check(h, "k_tuples");
   if (rc) return rc;
+  // one round trip in the common case: CS records + [n_hits | first kFirst hits]
+  const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
   CK(h, cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, s));
-  CK(h, cudaMemcpyAsync(h->h_cnt, D.n_hits, 8, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, s));
   CK(h, cudaStreamSynchronize(s));
-  const uint64_t total = h->h_cnt[0];
+  const uint64_t total = *(const unsigned long long*)h->h_res;
   const uint64_t got = std::min<uint64_t>(total, D.hit_cap);
-  if (got > h->h_hits_cap) {
-    cudaFreeHost(h->h_hits);
-    h->h_hits = nullptr;
-    h->h_hits_cap = std::max<uint64_t>(got, 2 * h->h_hits_cap);
-    CK(h, cudaMallocHost(&h->h_hits, h->h_hits_cap * sizeof(cbaa_host)));
-  }
-  if (got) {
-    CK(h, cudaMemcpyAsync(h->h_hits, D.hits, got * sizeof(cbaa_host), cudaMemcpyDeviceToHost, s));
+  if (got > kFirst) {
+    if (got > h->h_hits_cap) {
+      void* bigger = nullptr;
+      uint64_t cap2 = std::max<uint64_t>(got, 2 * h->h_hits_cap);
+      CK(h, cudaMallocHost(&bigger, 64 + cap2 * sizeof(cbaa_host)));
+      std::memcpy(bigger, h->h_res, 64 + kFirst * sizeof(cbaa_host));
+      cudaFreeHost(h->h_res);
+      h->h_res = bigger;
+      h->h_hits = (cbaa_host*)((char*)bigger + 64);
+      h->h_hits_cap = cap2;
+    }
+    CK(h, cudaMemcpyAsync(h->h_hits + kFirst, D.hits + kFirst, (got - kFirst) * sizeof(cbaa_host),
+                          cudaMemcpyDeviceToHost, s));
     CK(h, cudaStreamSynchronize(s));
   }
   // output order of S:418: estimate descending, then ip ascending

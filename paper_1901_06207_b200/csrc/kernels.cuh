@@ -217,21 +217,6 @@ __global__ void __launch_bounds__(kThreads) k_or_merge(uint4* __restrict__ dst, 
 }
 
 // ---------------------------------------------------------------- window-end detect
-// Zero bits of one column (g rows = wpc words), summed by one warp.
-__device__ __forceinline__ uint32_t column_popc(const Geo& G, const uint32_t* __restrict__ col, int lane) {
-  uint32_t pop = 0;
-  if ((G.wpc & 127u) == 0) {
-    const uint4* c4 = reinterpret_cast<const uint4*>(col);
-    for (uint32_t w = lane; w < (G.wpc >> 2); w += 32) {
-      uint4 v = __ldcg(c4 + w);
-      pop += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-    }
-  } else {
-    for (uint32_t w = lane; w < G.wpc; w += 32) pop += __popc(__ldcg(col + w));
-  }
-  return warp_sum(pop);
-}
-
 // Per-CS window math in fp64 (Q12, Thm. 1, θ_bn P:261 / Q15, Q16).
 __device__ void cs_math(const Geo& G, uint64_t ztot, uint32_t theta, cbaa_cs_stats* rec) {
   const double g = (double)G.g;
@@ -269,14 +254,40 @@ struct DetectScratch {
   uint64_t cand_cap;
 };
 
-// grid = n_range · num_ra · n_chunks CTAs; one warp per column; the last CTA of each CS finishes
-// that CS (math + ordered HC compaction); the last CS overall writes the tuple prefix.
+// Block-wide exclusive prefix sum of one value per thread; returns the block total in *total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    uint32_t c = s_warp[w];
+    before += w < warp ? c : 0u;
+    tot += c;
+  }
+  __syncthreads();
+  *total = tot;
+  return before + incl - v;
+}
+
+// grid = n_range · num_ra · n_chunks CTAs of 8 warps; each warp zero-counts columns c0+warp, c0+warp+8, …
+// with up to 8 column loads in flight (VEC: one 16-B load per lane per column, g = 4096).  The last CTA
+// of each CS finishes that CS (fp64 math + ordered Alg. 2 compaction); the last CS overall writes the
+// tuple-space prefix used by k_tuples.
+template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
                                                        const __grid_constant__ DetectScratch D, uint32_t cs_lo,
                                                        uint32_t n_range, uint32_t chunk, uint32_t n_chunks,
                                                        uint32_t theta, int finish) {
   __shared__ unsigned long long s_part[kWarps];
-  __shared__ uint32_t s_wcnt[kWarps];
+  __shared__ uint32_t s_warp[kWarps];
   __shared__ int s_last;
   __shared__ uint32_t s_zmax;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -288,12 +299,36 @@ __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ G
   unsigned long long part = 0;
   const uint32_t* arr = cube + (size_t)cs * G.cs_words + G.arr_off[i];
   uint32_t* zc = D.zc + (size_t)cs * G.ra_cols + G.ra_off[i];
-  for (uint32_t col = c0 + warp; col < c1; col += kWarps) {
-    uint32_t pop = column_popc(G, arr + ((size_t)col << G.wpc_log2), lane);
-    uint32_t z = G.g - pop;
-    if (lane == 0) {
-      zc[col] = z;
-      part += z;
+  if (finish && blockIdx.x == 0 && threadIdx.x == 0) *D.n_hits = 0;   // k_tuples runs after this grid
+  for (uint32_t base = c0 + warp; base < c1; base += 8 * kWarps) {
+    uint32_t pop[8];
+    if (VEC) {
+      uint4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t col = base + k * kWarps;
+        v[k] = col < c1 ? __ldcg(reinterpret_cast<const uint4*>(arr + ((size_t)col << G.wpc_log2)) + lane)
+                        : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pop[k] = __popc(v[k].x) + __popc(v[k].y) + __popc(v[k].z) + __popc(v[k].w);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t col = base + k * kWarps;
+        pop[k] = 0;
+        if (col < c1)
+          for (uint32_t w = lane; w < G.wpc; w += 32) pop[k] += __popc(__ldcg(arr + ((size_t)col << G.wpc_log2) + w));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t col = base + k * kWarps;
+      uint32_t z = G.g - warp_sum(pop[k]);   // zero bits of the column
+      if (lane == 0 && col < c1) {
+        zc[col] = z;
+        part += z;
+      }
     }
   }
   if (!finish) return;
@@ -322,26 +357,29 @@ __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ G
   const uint32_t* zcs = D.zc + (size_t)cs * G.ra_cols;
   uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
   unsigned long long prod = 1;
+  constexpr uint32_t kPer = 16;                        // columns per thread per tile, held in registers
   for (uint32_t a = 0; a < G.num_ra; ++a) {
-    uint32_t base = 0;
-    for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads) {
-      uint32_t col = t0 + threadIdx.x;
-      bool hot = col < G.ncols[a] && __ldcg(zcs + G.ra_off[a] + col) <= zmax;   // P:272, Q16
-      unsigned int b = __ballot_sync(0xffffffffu, hot);
-      if (lane == 0) s_wcnt[warp] = __popc(b);
-      __syncthreads();
-      uint32_t off = base, tot = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        uint32_t c = s_wcnt[w];
-        if (w < warp) off += c;
-        tot += c;
+    uint32_t written = 0;
+    const uint32_t* za = zcs + G.ra_off[a];
+    for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads * kPer) {
+      const uint32_t my0 = t0 + threadIdx.x * kPer;
+      uint32_t z[kPer];
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k) z[k] = my0 + k < G.ncols[a] ? __ldcg(za + my0 + k) : 0xffffffffu;
+      uint32_t flags = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k) flags |= (z[k] <= zmax ? 1u : 0u) << k;   // P:272, Q16
+      uint32_t tot;
+      uint32_t off = written + block_exclusive_scan(__popc(flags), s_warp, &tot);
+      while (flags) {
+        int k = __ffs(flags) - 1;
+        flags &= flags - 1;
+        hcs[G.ra_off[a] + off++] = my0 + k;
       }
-      if (hot) hcs[G.ra_off[a] + off + __popc(b & ((1u << lane) - 1u))] = col;
-      base += tot;
-      __syncthreads();
+      written += tot;
     }
-    if (threadIdx.x == 0) rec->n_hot[a] = base;
-    prod = (base != 0 && prod > ~0ull / base) ? ~0ull : prod * base;   // saturating ∏|HC(i)|
+    if (threadIdx.x == 0) rec->n_hot[a] = written;
+    prod = (written != 0 && prod > ~0ull / written) ? ~0ull : prod * written;   // saturating ∏|HC(i)|
   }
   if (threadIdx.x == 0) {
     rec->tuples = prod;
