@@ -37,11 +37,42 @@ class WindowSpec:
     pareto_max: float = 1.0e4    # truncation of the tail weight
     order: str = "shuffled"      # "shuffled" (primary) | "bursty" (each flow's packets contiguous)
     n_prefixes: int = 16         # random /16 prefixes forming NI
+    victim_share: float = 0.0    # if > 0: fraction of the window's packets that go to the DDoS victims
 
 
 # BASELINE.json configs.
 C1 = WindowSpec(n=1_000_000, n_hosts=49_980, n_flows=400_000, card_cap=500, scanners=(2000,) * 20)
 C2 = WindowSpec(n=100_000_000, n_hosts=600_000, n_flows=9_000_000)
+# Config 3: four edge routers, 50M packets each, of one C2-like flow set (router k: packet_seed = k + 1).
+C3_ROUTER = WindowSpec(n=50_000_000, n_hosts=600_000, n_flows=9_000_000)
+C3_ROUTERS = 4
+
+
+def c4_spec(n_shard=250_000_000, scale=1.0, seed=4):
+    """Config 4: one shard (of 8) of the 2B-pair window: 16M Zipf flows over 1.2M hosts, 50 scanners
+    (d ~ U[2K, 20K]), 20 DDoS victims (d ~ U[5K, 30K]) that receive ~5% of the packets.  `scale`
+    shrinks hosts/flows/packets for the reduced parity test."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    sc = tuple(int(x) for x in rng.integers(2000, 20001, 50))
+    vi = tuple(int(x) for x in rng.integers(5000, 30001, 20))
+    return WindowSpec(n=int(n_shard * scale), n_hosts=int(1_200_000 * scale), n_flows=int(16_000_000 * scale),
+                      scanners=sc, victims=vi, victim_share=0.05)
+
+
+def c5_geometries():
+    """Config 5 grid (SURVEY §8(d)): r ∈ {2,4,6} × g ∈ {1024..8192} × cbn ∈ {10,12,14}, |RA| = 3, |VA| = 1;
+    clbs = [0,10,20] at the paper point (r=4, cbn=12), else clbs(i) = round(i·L/|RA|)."""
+    out = []
+    for r in (2, 4, 6):
+        L = 32 - r
+        for cbn in (10, 12, 14):
+            clbs = [0, 10, 20] if (r, cbn) == (4, 12) else [int(round(i * L / 3)) for i in range(3)]
+            for g in (1024, 2048, 4096, 8192):
+                out.append(dict(r=r, g=g, cbn=[cbn] * 4, clbs=clbs))
+    return out
+
+
+C5_THETAS = (256, 512, 1024, 2048, 4096, 8192)
 
 
 def c5_spec(seed_rng: np.random.Generator | None = None, n=500_000_000):
@@ -121,10 +152,21 @@ def generate(spec: WindowSpec, seed: int, packet_seed: int | None = None, n: int
         h = planted_hosts[len(spec.scanners) + k]
         planted[int(h)] = int(d)
         p_inner.append(np.full(d, h, np.uint32)); p_outer.append(_distinct_outer(rng, d, pre16))
-        p_pk.append(rng.integers(1, 4, size=d).astype(np.int64)); p_victim.append(np.ones(d, bool))
+        p_pk.append(None if spec.victim_share > 0 else rng.integers(1, 4, size=d).astype(np.int64))
+        p_victim.append(np.ones(d, bool))
 
     # ---- packets: everything below depends on packet_seed only
     prng = _rng(seed if packet_seed is None else packet_seed)
+    if spec.victim_share > 0 and spec.victims:
+        # victims' flows share victim_share·n packets: one each, the rest multinomially (a flood)
+        nv = sum(spec.victims)
+        extra_v = max(0, int(spec.victim_share * n) - nv)
+        vk = 1 + prng.multinomial(extra_v, np.full(nv, 1.0 / nv))
+        off = 0
+        for k in range(len(spec.scanners), len(p_pk)):
+            d = spec.victims[k - len(spec.scanners)]
+            p_pk[k] = vk[off:off + d]
+            off += d
     pk_planted = np.concatenate(p_pk) if p_pk else np.zeros(0, np.int64)
     n_bg = n - int(pk_planted.sum())
     if n_bg < n_bg_flows:

@@ -15,7 +15,7 @@ __device__ __forceinline__ uint32_t hmix(uint32_t h) {
 }
 
 // mode 0: RED.OR random word; 1: RED with L2 evict_last hint; 2: LDG random word;
-// 3: ATOM.OR with return (forces round trip)
+// 3: ATOM.OR with return (forces round trip); 4: LDG through L1 (ld.global.ca)
 template <int MODE>
 __global__ void k_rand(uint32_t* buf, uint32_t words_mask, uint64_t ops_per_thread, uint32_t seed, uint32_t* sink) {
   uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -35,6 +35,10 @@ __global__ void k_rand(uint32_t* buf, uint32_t words_mask, uint64_t ops_per_thre
       } else if (MODE == 2) {
         uint32_t v;
         asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(buf + w));
+        acc += v;
+      } else if (MODE == 4) {
+        uint32_t v;
+        asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(buf + w));
         acc += v;
       } else {
         acc += atomicOr(buf + w, m);
@@ -88,16 +92,17 @@ int main(int argc, char** argv) {
   int blocks = sms * 8, threads = 256;
   uint64_t nthreads = (uint64_t)blocks * threads;
   const uint64_t opt = 1024;  // ops per thread
-  uint64_t sizes_mb[] = {4, 16, 32, 64, 96, 128, 256, 1024};
-  const char* names[] = {"red", "red_evict_last", "ldg", "atom_ret"};
+  uint64_t sizes_kb[] = {16, 128, 1024, 4096, 16384, 32768, 65536, 98304, 131072, 262144, 1048576};
+  const char* names[] = {"red", "red_evict_last", "ldg", "atom_ret", "ldg_ca"};
   if (quick) {  // roofline denominators: random single-word RED.OR and LDG over an L2-resident 64 MiB buffer
     const uint32_t mask = (uint32_t)((64ull << 20) / 4) - 1;
-    for (int mode = 0; mode < 3; mode += 2) {
+    for (int mode : {0, 2, 4}) {
       float best = 1e30f;
       for (int rep = 0; rep < 6; ++rep) {
         cudaEventRecord(e0);
         if (mode == 0) k_rand<0><<<blocks, threads>>>(buf, mask, opt, rep, sink);
-        else k_rand<2><<<blocks, threads>>>(buf, mask, opt, rep, sink);
+        else if (mode == 2) k_rand<2><<<blocks, threads>>>(buf, mask, opt, rep, sink);
+        else k_rand<4><<<blocks, threads>>>(buf, mask, opt, rep, sink);
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (rep > 0 && ms < best) best = ms;
@@ -107,9 +112,9 @@ int main(int argc, char** argv) {
     }
     return 0;
   }
-  for (int mode = 0; mode < 4; ++mode) {
-    for (uint64_t mb : sizes_mb) {
-      uint32_t words = (uint32_t)((mb << 20) / 4);
+  for (int mode = 0; mode < 5; ++mode) {
+    for (uint64_t kb : sizes_kb) {
+      uint32_t words = (uint32_t)((kb << 10) / 4);
       uint32_t mask = words - 1;
       float best = 1e30f;
       for (int rep = 0; rep < 4; ++rep) {
@@ -118,13 +123,14 @@ int main(int argc, char** argv) {
         if (mode == 1) k_rand<1><<<blocks, threads>>>(buf, mask, opt, rep, sink);
         if (mode == 2) k_rand<2><<<blocks, threads>>>(buf, mask, opt, rep, sink);
         if (mode == 3) k_rand<3><<<blocks, threads>>>(buf, mask, opt, rep, sink);
+        if (mode == 4) k_rand<4><<<blocks, threads>>>(buf, mask, opt, rep, sink);
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (rep > 0 && ms < best) best = ms;
       }
       double ops = (double)nthreads * opt;
-      printf("{\"mode\": \"%s\", \"buf_mb\": %llu, \"ms\": %.4f, \"Gops\": %.2f}\n", names[mode],
-             (unsigned long long)mb, best, ops / best / 1e6);
+      printf("{\"mode\": \"%s\", \"buf_kb\": %llu, \"ms\": %.4f, \"Gops\": %.2f}\n", names[mode],
+             (unsigned long long)kb, best, ops / best / 1e6);
     }
   }
   // stream + RED: 100M pairs (800 MB) into a 128 MiB cube, like C2
