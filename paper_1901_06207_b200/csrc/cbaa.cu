@@ -405,8 +405,9 @@ int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
   if (cfg->update_passes) {
     h->passes = cfg->update_passes;
   } else {
+    // capped at 8: past that the input re-reads cost more than the L2 misses they avoid
     double budget = 0.70 * (h->l2_bytes > 0 ? h->l2_bytes : (96 << 20));
-    h->passes = (uint32_t)std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget));
+    h->passes = (uint32_t)std::min<double>(8.0, std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget)));
   }
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
