@@ -190,6 +190,36 @@ int cbaa_detect(cbaa_handle* h, uint32_t theta, cbaa_host* out, uint64_t cap, ui
 int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t cs_hi, cbaa_host* out,
                       uint64_t cap, uint64_t* n_out, cbaa_cs_stats* stats, cbaa_stream stream);
 
+/* ------------------------------------------------------- SketchFile "CBA1"
+ * The transport of a local CBA to the global server ("each local server
+ * will send its CBA"), in SPEC's exact wire format (little-
+ * endian): "CBA1", u16 version = 1, u8 r, u8 num_ra, u8 num_va, u32 g,
+ * (num_ra+num_va) × u8 cbn, num_ra × u8 clbs, u32 mangle_a, u32 mangle_b,
+ * u32 bv_seed, num_va × u32 va_seeds, u64 payload bytes, payload = the cube in
+ * the byte layout above.  θ formula, tuple cap and direction are not part of a
+ * sketch's identity and are not stored. */
+#define CBAA_SKETCH_REPLACE 0  /* cube := file payload            */
+#define CBAA_SKETCH_MERGE 1    /* cube |= file payload     */
+
+/* Size in bytes of the SketchFile of this handle's cube. */
+uint64_t cbaa_sketch_bytes(const cbaa_handle* h);
+
+/* Writes the SketchFile into the HOST buffer out (cap bytes); *n_written = size.
+ * Returns CBAA_E_CAPACITY (and the required size) if cap is too small.
+ * Synchronizes stream (the cube is read after earlier work on it). */
+int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream);
+
+/* Parses a SketchFile header from HOST bytes into *out (other fields default).
+ * No GPU needed.  CBAA_E_CONFIG with last-error-style text in err (errlen bytes)
+ * names the bad field: magic, version, a geometry invariant, or the payload length. */
+int cbaa_sketch_config(const void* in, uint64_t n, cbaa_config* out, char* err, uint64_t errlen);
+
+/* Loads (REPLACE) or OR-merges (MERGE) a HOST SketchFile into the cube.  The
+ * header must match this handle's geometry and seeds exactly; otherwise
+ * CBAA_E_MISMATCH and last_error names the first differing field.
+ * Returns after the payload has been copied (the host buffer may be reused). */
+int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_stream stream);
+
 /* ---------------------------------------------------------------- inspection */
 
 /* Device pointer and size of the cube (for NCCL exchange and parity dumps). */

@@ -302,3 +302,39 @@ def candidates(p, cube, cs, zmax_, cap=1 << 22) -> np.ndarray:
 
 def lp_roundtrip_failures(p, lo, hi, flip_cp=False) -> int:
     return lib().orc_lp_roundtrip_failures(C.byref(to_struct(p)), lo, hi, int(flip_cp))
+
+
+# ----------------------------------------------------------------- SketchFile "CBA1"
+def serialize(p, cube: np.ndarray) -> bytes:
+    """SPEC's wire format, little-endian: magic "CBA1", u16 version 1, u8 r, u8 numRa, u8 numVa, u32 g,
+    (numRa+numVa) × u8 cbn, numRa × u8 clbs, u32 mangleA, u32 mangleB, u32 bvSeed, numVa × u32 vaSeeds,
+    u64 payload length, payload."""
+    import struct
+    narr = p["num_ra"] + p["num_va"]
+    head = b"CBA1" + struct.pack("<HBBBI", 1, p["r"], p["num_ra"], p["num_va"], p["g"])
+    head += bytes(p["cbn"][:narr]) + bytes(p["clbs"][: p["num_ra"]])
+    head += struct.pack("<III", p["mangle_a"], p["mangle_b"], p["bv_seed"])
+    head += struct.pack("<" + "I" * p["num_va"], *p["va_seeds"][: p["num_va"]])
+    head += struct.pack("<Q", cube.size)
+    return head + cube.tobytes()
+
+
+def deserialize(data: bytes):
+    """Inverse of serialize: (params dict of the sketch's identity, cube bytes)."""
+    import struct
+    if data[:4] != b"CBA1":
+        raise ValueError("bad magic")
+    version, r, nra, nva, g = struct.unpack_from("<HBBBI", data, 4)
+    if version != 1:
+        raise ValueError("bad version")
+    off = 13
+    cbn = list(data[off: off + nra + nva]); off += nra + nva
+    clbs = list(data[off: off + nra]); off += nra
+    a, b, bv = struct.unpack_from("<III", data, off); off += 12
+    vs = list(struct.unpack_from("<" + "I" * nva, data, off)); off += 4 * nva
+    (plen,) = struct.unpack_from("<Q", data, off); off += 8
+    if len(data) - off != plen:
+        raise ValueError(f"payload length {len(data) - off} != {plen}")
+    p = dict(default_params(), r=r, num_ra=nra, num_va=nva, g=g, cbn=cbn, clbs=clbs, mangle_a=a, mangle_b=b,
+             bv_seed=bv, va_seeds=vs)
+    return p, np.frombuffer(data, dtype=np.uint8, offset=off).copy()

@@ -22,6 +22,7 @@ E_CONFIG, E_ARG, E_CUDA, E_MISMATCH, E_CAPACITY, E_TUPLE_CAP, E_NOMEM = -1, -2, 
 THETA_PAPER, THETA_INVERTED = 0, 1
 DIR_NORMALIZED, DIR_INNER_PREFIX = 0, 1
 UPDATE_TEST_SET, UPDATE_RED = 0, 1
+SKETCH_REPLACE, SKETCH_MERGE = 0, 1
 
 
 class Config(C.Structure):
@@ -85,6 +86,10 @@ _SIGS = {
     "cbaa_candidates": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
     "cbaa_debug_map": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),
+    "cbaa_sketch_bytes": (C.c_uint64, [_h]),
+    "cbaa_serialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
+    "cbaa_sketch_config": (C.c_int, [C.c_void_p, C.c_uint64, _P(Config), C.c_char_p, C.c_uint64]),
+    "cbaa_deserialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]),
     "cbaa_kernel_launches": (C.c_uint64, [_h]),
     "cbaa_update_passes": (C.c_uint32, [_h]),
     "cbaa_strerror": (C.c_char_p, [C.c_int]),
@@ -152,6 +157,18 @@ def validate(cfg: Config):
 
 def cube_bytes(cfg: Config) -> int:
     return lib().cbaa_cube_bytes(C.byref(cfg))
+
+
+def sketch_config(data: bytes):
+    """Geometry and seeds of a SketchFile "CBA1"; raises CbaaError naming the bad field."""
+    c = Config()
+    err = C.create_string_buffer(256)
+    buf = C.create_string_buffer(bytes(data), len(data)) if not isinstance(data, np.ndarray) else None
+    ptr = C.cast(buf, C.c_void_p) if buf is not None else C.c_void_p(data.ctypes.data)
+    rc = lib().cbaa_sketch_config(ptr, len(data), C.byref(c), err, 256)
+    if rc != OK:
+        raise CbaaError(rc, "SketchFile: " + err.value.decode())
+    return c
 
 
 def _stream(stream):
@@ -325,6 +342,24 @@ class Cbaa:
                                          C.c_void_p(cols.data_ptr()), C.c_void_p(row.data_ptr()), _stream(stream)),
                     "cbaa_debug_map")
         return cs, cols.view(n, narr), row
+
+    # ------------------------------------------------------------ SketchFile
+    def serialize(self, stream=None) -> np.ndarray:
+        """The cube as a SketchFile "CBA1", uint8 numpy array."""
+        n = lib().cbaa_sketch_bytes(self._h)
+        out = np.empty(n, dtype=np.uint8)
+        w = C.c_uint64()
+        self._check(lib().cbaa_serialize(self._h, out.ctypes.data_as(C.c_void_p), n, C.byref(w), _stream(stream)),
+                    "cbaa_serialize")
+        return out
+
+    def deserialize(self, data, merge: bool = False, stream=None):
+        """Load (or OR-merge) a SketchFile into the cube; refuses a different geometry/seeds."""
+        a = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+        a = np.ascontiguousarray(a)
+        self._check(lib().cbaa_deserialize(self._h, a.ctypes.data_as(C.c_void_p), a.size,
+                                           SKETCH_MERGE if merge else SKETCH_REPLACE, _stream(stream)),
+                    "cbaa_deserialize")
 
     @property
     def kernel_launches(self) -> int:

@@ -707,6 +707,169 @@ int cbaa_debug_map(cbaa_handle* h, const uint32_t* iip, const uint32_t* oip, uin
   return launch_check(h, "k_debug_map");
 }
 
+// ------------------------------------------------------------------ SketchFile "CBA1"
+static uint64_t sketch_header_bytes(const cbaa_config& c) {
+  return 4 + 2 + 3 + 4 + (c.num_ra + c.num_va) + c.num_ra + 12 + 4ull * c.num_va + 8;
+}
+
+uint64_t cbaa_sketch_bytes(const cbaa_handle* h) {
+  return h ? sketch_header_bytes(h->cfg) + h->cube_bytes : 0;
+}
+
+namespace {
+struct Writer {
+  uint8_t* p;
+  void u8(uint32_t v) { *p++ = (uint8_t)v; }
+  void u16(uint32_t v) { u8(v & 0xff); u8(v >> 8); }
+  void u32(uint32_t v) { for (int k = 0; k < 4; ++k) u8((v >> (8 * k)) & 0xff); }
+  void u64(uint64_t v) { for (int k = 0; k < 8; ++k) u8((uint32_t)((v >> (8 * k)) & 0xff)); }
+};
+struct Reader {
+  const uint8_t* p;
+  const uint8_t* end;
+  bool ok = true;
+  uint32_t u8() {
+    if (p >= end) { ok = false; return 0; }
+    return *p++;
+  }
+  uint32_t u16() { uint32_t a = u8(); return a | (u8() << 8); }
+  uint32_t u32() { uint32_t v = 0; for (int k = 0; k < 4; ++k) v |= u8() << (8 * k); return v; }
+  uint64_t u64() { uint64_t v = 0; for (int k = 0; k < 8; ++k) v |= (uint64_t)u8() << (8 * k); return v; }
+};
+
+// Parses the header; on success *payload points at the cube bytes and *plen is their length.
+int parse_sketch(const void* in, uint64_t n, cbaa_config* out, const uint8_t** payload, uint64_t* plen,
+                 std::string* why) {
+  auto bad = [&](const std::string& m) {
+    if (why) *why = m;
+    return CBAA_E_CONFIG;
+  };
+  if (!in || !out) return bad("null buffer");
+  Reader R{(const uint8_t*)in, (const uint8_t*)in + n};
+  char magic[4];
+  for (int k = 0; k < 4; ++k) magic[k] = (char)R.u8();
+  if (!R.ok || std::memcmp(magic, "CBA1", 4) != 0) return bad("magic: expected \"CBA1\"");
+  uint32_t version = R.u16();
+  if (!R.ok || version != 1) return bad("version: expected 1");
+  cbaa_config c;
+  cbaa_config_default(&c);
+  c.r = R.u8();
+  c.num_ra = R.u8();
+  c.num_va = R.u8();
+  c.g = R.u32();
+  if (!R.ok) return bad("header truncated");
+  if (c.num_ra > CBAA_MAX_RA || c.num_va > CBAA_MAX_VA) return bad("num_ra/num_va out of range");
+  std::memset(c.cbn, 0, sizeof c.cbn);
+  std::memset(c.clbs, 0, sizeof c.clbs);
+  std::memset(c.va_seeds, 0, sizeof c.va_seeds);
+  for (uint32_t a = 0; a < c.num_ra + c.num_va; ++a) c.cbn[a] = (uint8_t)R.u8();
+  for (uint32_t i = 0; i < c.num_ra; ++i) c.clbs[i] = (uint8_t)R.u8();
+  c.mangle_a = R.u32();
+  c.mangle_b = R.u32();
+  c.bv_seed = R.u32();
+  for (uint32_t j = 0; j < c.num_va; ++j) c.va_seeds[j] = R.u32();
+  uint64_t len = R.u64();
+  if (!R.ok) return bad("header truncated");
+  std::string inv;
+  if (validate(&c, &inv)) return bad("config invariant: " + inv);
+  uint64_t want = cbaa_cube_bytes(&c);
+  if (len != want)
+    return bad("payload length field " + std::to_string(len) + " != cube size " + std::to_string(want));
+  uint64_t have = (uint64_t)(R.end - R.p);
+  if (have < len)
+    return bad("payload truncated: expected " + std::to_string(len) + " bytes, got " + std::to_string(have));
+  *out = c;
+  if (payload) *payload = R.p;
+  if (plen) *plen = len;
+  return CBAA_OK;
+}
+}  // namespace
+
+int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream) {
+  if (!h || !n_written) return CBAA_E_ARG;
+  const cbaa_config& c = h->cfg;
+  const uint64_t hb = sketch_header_bytes(c), total = hb + h->cube_bytes;
+  *n_written = total;
+  if (cap < total || !out) return fail(h, CBAA_E_CAPACITY, "cbaa_serialize: buffer smaller than cbaa_sketch_bytes");
+  DeviceGuard dg(h->device);
+  Writer W{(uint8_t*)out};
+  W.u8('C'); W.u8('B'); W.u8('A'); W.u8('1');
+  W.u16(1);
+  W.u8(c.r); W.u8(c.num_ra); W.u8(c.num_va);
+  W.u32(c.g);
+  for (uint32_t a = 0; a < c.num_ra + c.num_va; ++a) W.u8(c.cbn[a]);
+  for (uint32_t i = 0; i < c.num_ra; ++i) W.u8(c.clbs[i]);
+  W.u32(c.mangle_a); W.u32(c.mangle_b); W.u32(c.bv_seed);
+  for (uint32_t j = 0; j < c.num_va; ++j) W.u32(c.va_seeds[j]);
+  W.u64(h->cube_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaMemcpyAsync((uint8_t*)out + hb, h->cube, h->cube_bytes, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  return CBAA_OK;
+}
+
+int cbaa_sketch_config(const void* in, uint64_t n, cbaa_config* out, char* err, uint64_t errlen) {
+  std::string why;
+  int rc = parse_sketch(in, n, out, nullptr, nullptr, &why);
+  if (err && errlen) std::snprintf(err, (size_t)errlen, "%s", rc ? why.c_str() : "");
+  return rc;
+}
+
+int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (mode != CBAA_SKETCH_REPLACE && mode != CBAA_SKETCH_MERGE) return fail(h, CBAA_E_ARG, "bad mode");
+  cbaa_config fc;
+  const uint8_t* payload = nullptr;
+  uint64_t plen = 0;
+  std::string why;
+  if (parse_sketch(in, n, &fc, &payload, &plen, &why)) return fail(h, CBAA_E_CONFIG, "SketchFile: " + why);
+  const cbaa_config& c = h->cfg;
+  auto mismatch = [&](const char* field) {
+    return fail(h, CBAA_E_MISMATCH, std::string("SketchFile refused: field '") + field + "' differs from this cube");
+  };
+  if (fc.r != c.r) return mismatch("r");
+  if (fc.num_ra != c.num_ra) return mismatch("num_ra");
+  if (fc.num_va != c.num_va) return mismatch("num_va");
+  if (fc.g != c.g) return mismatch("g");
+  for (uint32_t a = 0; a < c.num_ra + c.num_va; ++a)
+    if (fc.cbn[a] != c.cbn[a]) return mismatch("cbn");
+  for (uint32_t i = 0; i < c.num_ra; ++i)
+    if (fc.clbs[i] != c.clbs[i]) return mismatch("clbs");
+  if (fc.mangle_a != c.mangle_a) return mismatch("mangle_a");
+  if (fc.mangle_b != c.mangle_b) return mismatch("mangle_b");
+  if (fc.bv_seed != c.bv_seed) return mismatch("bv_seed");
+  for (uint32_t j = 0; j < c.num_va; ++j)
+    if (fc.va_seeds[j] != c.va_seeds[j]) return mismatch("va_seeds");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (mode == CBAA_SKETCH_REPLACE) {
+    CK(h, cudaMemcpyAsync(h->cube, payload, plen, cudaMemcpyHostToDevice, s));
+    CK(h, cudaStreamSynchronize(s));
+    return CBAA_OK;
+  }
+  // MERGE: stage the payload on the device in 64 MiB slices and OR them in
+  const uint64_t slice = 64ull << 20;
+  void* stage = nullptr;
+  CK(h, cudaMalloc(&stage, std::min(slice, plen)));
+  int rc = CBAA_OK;
+  for (uint64_t off = 0; off < plen && rc == CBAA_OK; off += slice) {
+    const uint64_t m = std::min(slice, plen - off);
+    cudaError_t e = cudaMemcpyAsync(stage, payload + off, m, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { rc = cuda_fail(h, e, "cudaMemcpyAsync(sketch payload)"); break; }
+    MergeSrcs S{};
+    S.k = 1;
+    S.p[0] = (const uint4*)stage;
+    k_or_merge<<<grid_for(h, m / 16, 4), kThreads, 0, s>>>((uint4*)((char*)h->cube + off), S, m / 16);
+    rc = launch_check(h, "k_or_merge(sketch)");
+    if (rc == CBAA_OK) {
+      e = cudaStreamSynchronize(s);   // the staging slice is reused by the next copy
+      if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaStreamSynchronize");
+    }
+  }
+  cudaFree(stage);
+  return rc;
+}
+
 uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0; }
 
 uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }

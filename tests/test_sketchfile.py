@@ -1,0 +1,80 @@
+"""SketchFile "CBA1": the cross-router transport of a local CBA.
+
+CPU tests: the library's header parser against the oracle's serializer (written separately from S:479).
+GPU tests: device cube → file bytes identical to the oracle's file; REPLACE / MERGE round trips;
+globalMerge of router files == the oracle cube of the whole stream; refusals name the field."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1901_06207_b200 import cbaa as cb
+from paper_1901_06207_b200 import workload as W
+from tests.geometries import random_params
+
+
+def test_header_parse_matches_oracle_serializer(paper):
+    for p in [paper] + [random_params(s) for s in range(10)]:
+        data = O.serialize(p, np.zeros(O.cube_bytes(p), np.uint8))
+        c = cb.sketch_config(data)
+        d = c.to_dict()
+        for k in ("r", "num_ra", "num_va", "g", "cbn", "clbs", "mangle_a", "mangle_b", "bv_seed", "va_seeds"):
+            assert d[k] == p[k], k
+
+
+def test_paper_geometry_file_size(paper):
+    """the paper-config sketch is exactly 128 MiB of payload."""
+    data = O.serialize(paper, np.zeros(O.cube_bytes(paper), np.uint8))
+    assert len(data) - (1 << 27) == 4 + 2 + 3 + 4 + 4 + 3 + 12 + 4 + 8
+
+
+@pytest.mark.parametrize("mutate, field", [
+    (lambda b: b"XBA1" + b[4:], "magic"),
+    (lambda b: b[:4] + b"\x02\x00" + b[6:], "version"),
+    (lambda b: b[:-1], "payload truncated"),
+    (lambda b: b[:20], "truncated"),
+])
+def test_header_errors_name_the_field(paper, mutate, field):
+    p = dict(paper, r=8, g=32, cbn=[9, 9, 9, 8], clbs=[0, 8, 16])
+    data = O.serialize(p, np.zeros(O.cube_bytes(p), np.uint8))
+    with pytest.raises(cb.CbaaError) as e:
+        cb.sketch_config(mutate(data))
+    assert field in str(e.value)
+
+
+def test_oracle_roundtrip(paper):
+    p = dict(paper, r=8, g=64, cbn=[9, 9, 9, 8], clbs=[0, 8, 16])
+    src, dst = W.random_pairs(5000, 3)
+    cube, _ = O.update(p, src, dst)
+    q, back = O.deserialize(O.serialize(p, cube))
+    assert np.array_equal(back, cube) and q["va_seeds"] == p["va_seeds"]
+
+
+@pytest.mark.gpu
+def test_gpu_file_equals_oracle_file_and_global_merge(paper):
+    import torch
+    from tests.test_gpu_parity import dev, gpu_cube, handle
+    w = W.generate(W.WindowSpec(n=400_000, n_hosts=8000, n_flows=50000, scanners=(2000,) * 3), 12)
+    part = W.partition(w.src.size, 4, "hash-by-pair", w.src, w.dst)
+    files = []
+    for k in range(4):
+        sel = part == k
+        h = handle(paper)
+        h.reset()
+        h.update(dev(w.src[sel]), dev(w.dst[sel]))
+        f = h.serialize()
+        ref, _ = O.update(paper, w.src[sel], w.dst[sel])
+        assert f.tobytes() == O.serialize(paper, ref)            # device file == oracle file, byte for byte
+        files.append(f)
+    g = handle(paper)
+    g.reset()
+    for f in files:
+        g.deserialize(f, merge=True)                             # globalMerge
+    whole, _ = O.update(paper, w.src, w.dst)
+    assert np.array_equal(gpu_cube(g), whole)
+    r = handle(paper)
+    r.deserialize(files[0])                                      # REPLACE
+    assert np.array_equal(gpu_cube(r), np.frombuffer(files[0].tobytes()[-(1 << 27):], np.uint8))
+    other = handle(dict(paper, bv_seed=paper["bv_seed"] ^ 1))
+    with pytest.raises(cb.CbaaError) as e:
+        other.deserialize(files[0], merge=True)
+    assert e.value.code == cb.E_MISMATCH and "bv_seed" in str(e.value)
