@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
     ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
+    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or NVLink pull-OR over symmetric memory")
     return ap.parse_args()
 
 
@@ -213,7 +215,16 @@ def main():
     cfg = default_config()
     cfg.update_passes = args.passes
     cfg.update_mode = 0 if args.update_mode == "test_set" else 1
-    cb = Cbaa(cfg, local)
+    from paper_1901_06207_b200.cbaa import cube_bytes
+    peer = None
+    exchange = args.exchange if world > 1 else "none"
+    if exchange == "p2p":
+        try:
+            peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", local))
+        except Exception as e:   # no symmetric memory on this box: say so and use NCCL
+            print(f"[bench] p2p exchange unavailable ({e}); using nccl", file=sys.stderr)
+            exchange = "nccl"
+    cb = Cbaa(cfg, local, cube=peer.buf if peer else None)
     n_cs = cb.n_cs
     cs_bytes = cb.nbytes // n_cs
     stream = torch.cuda.Stream()
@@ -232,8 +243,14 @@ def main():
         lo, hi = 0, n_cs
         if world > 1:
             with torch.cuda.stream(stream):
-                lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
+                if peer:
+                    lo, hi = peer.exchange(cb, rank, world, n_cs, cs_bytes, stream)
+                else:
+                    lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
         hosts, stats, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream)
+        if peer:
+            with torch.cuda.stream(stream):
+                peer.window_done()
         if ev:
             ev[2].record(stream)
         return D.gather_hosts(hosts, rank, world)
@@ -335,7 +352,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config_block(args.workload, spec, world),
+            "config": dict(config_block(args.workload, spec, world), exchange=exchange),
             "detect_ms": statistics.median(det_ms), "update_ms": upd,
             "post_update_ms": statistics.median(post_ms),
             "update_pairs_per_s": n * world / (upd / 1e3),

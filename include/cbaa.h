@@ -136,6 +136,12 @@ uint64_t cbaa_cube_bytes(const cbaa_config* cfg);
 /* Validates cfg, selects `device`, allocates the cube (zeroed) and all detect
  * scratch.  *out owns everything until cbaa_destroy. */
 int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out);
+
+/* Same, but the cube lives in caller-owned DEVICE memory `cube` (≥ cube_bytes,
+ * 256-byte aligned), e.g. a symmetric-memory buffer that peer GPUs map over
+ * NVLink so cbaa_merge_slice can pull their slices directly.
+ * The memory is zeroed here and never freed by the library. */
+int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cube_nbytes, cbaa_handle** out);
 void cbaa_destroy(cbaa_handle* h);
 int cbaa_get_config(const cbaa_handle* h, cbaa_config* out);
 

@@ -68,6 +68,7 @@ _SIGS = {
     "cbaa_config_validate": (C.c_int, [_P(Config), C.c_char_p, C.c_uint64]),
     "cbaa_cube_bytes": (C.c_uint64, [_P(Config)]),
     "cbaa_create": (C.c_int, [_P(Config), C.c_int, _P(C.c_void_p)]),
+    "cbaa_create_ext": (C.c_int, [_P(Config), C.c_int, C.c_void_p, C.c_uint64, _P(C.c_void_p)]),
     "cbaa_destroy": (None, [_h]),
     "cbaa_get_config": (C.c_int, [_h, _P(Config)]),
     "cbaa_reset": (C.c_int, [_h, C.c_void_p]),
@@ -192,15 +193,21 @@ def _dptr(t, what):
 class Cbaa:
     """One cube of bits arrays on one GPU (a local server's CBA)."""
 
-    def __init__(self, cfg: Config | dict | None = None, device: int = 0):
+    def __init__(self, cfg: Config | dict | None = None, device: int = 0, cube=None):
+        """cube: optional caller-owned uint8 CUDA tensor (e.g. torch symmetric memory) to hold the cube."""
         if cfg is None:
             cfg = default_config()
         elif isinstance(cfg, dict):
             cfg = config_from_dict(cfg)
         self.cfg = cfg
         self.device = device
+        self._ext = cube          # keeps caller memory alive as long as the handle
         h = C.c_void_p()
-        rc = lib().cbaa_create(C.byref(cfg), device, C.byref(h))
+        if cube is None:
+            rc = lib().cbaa_create(C.byref(cfg), device, C.byref(h))
+        else:
+            rc = lib().cbaa_create_ext(C.byref(cfg), device, C.c_void_p(cube.data_ptr()),
+                                       cube.numel() * cube.element_size(), C.byref(h))
         if rc != OK:
             raise CbaaError(rc, "cbaa_create failed: " + validate(cfg)[1])
         self._h = h
@@ -263,7 +270,9 @@ class Cbaa:
         self._check(lib().cbaa_merge(self._h, arr, len(ptrs), self.nbytes, _stream(stream)), "cbaa_merge")
 
     def merge_slice(self, slices, cs_lo, cs_hi, stream=None):
-        ptrs = [s.data_ptr() for s in slices]
+        """OR the bytes of CSs [cs_lo, cs_hi) of peer cubes into this cube: each slice is a uint8 CUDA
+        tensor or a raw device address (e.g. a peer's symmetric-memory pointer, read over NVLink)."""
+        ptrs = [s if isinstance(s, int) else s.data_ptr() for s in slices]
         arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
         self._check(lib().cbaa_merge_slice(self._h, arr, len(ptrs), cs_lo, cs_hi, _stream(stream)),
                     "cbaa_merge_slice")

@@ -26,6 +26,7 @@ struct cbaa_handle {
   int l2_bytes = 0;
   uint32_t passes = 1;
   uint32_t* cube = nullptr;
+  bool cube_external = false;   // cube memory owned by the caller (cbaa_create_ext)
   uint64_t cube_bytes = 0;
   uint64_t cube_words = 0;
   // detect scratch (one allocation, see alloc_scratch)
@@ -364,7 +365,7 @@ uint64_t cbaa_cube_bytes(const cbaa_config* cfg) {
   return (csb << cfg->r) / 8;
 }
 
-int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
+int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cube_nbytes, cbaa_handle** out) {
   if (!out) return CBAA_E_ARG;
   *out = nullptr;
   std::string why;
@@ -388,8 +389,18 @@ int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
   h->cube_bytes = cbaa_cube_bytes(cfg);
   h->cube_words = h->cube_bytes / 4;
   int rc = CBAA_OK;
-  cudaError_t e = cudaMalloc(&h->cube, h->cube_bytes);
-  if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMalloc(cube)");
+  cudaError_t e = cudaSuccess;
+  if (cube) {   // caller-owned cube, e.g. a symmetric-memory buffer peers map over NVLink
+    if (cube_nbytes < h->cube_bytes || ((uintptr_t)cube & 255)) {
+      delete h;
+      return CBAA_E_ARG;
+    }
+    h->cube = (uint32_t*)cube;
+    h->cube_external = true;
+  } else {
+    e = cudaMalloc(&h->cube, h->cube_bytes);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMalloc(cube)");
+  }
   if (!rc) {
     e = cudaMemset(h->cube, 0, h->cube_bytes);
     if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemset(cube)");
@@ -416,10 +427,14 @@ int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
   return CBAA_OK;
 }
 
+int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out) {
+  return cbaa_create_ext(cfg, device, nullptr, 0, out);
+}
+
 void cbaa_destroy(cbaa_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->device);
-  if (h->cube) cudaFree(h->cube);
+  if (h->cube && !h->cube_external) cudaFree(h->cube);
   if (h->scratch) cudaFree(h->scratch);
   if (h->D.cand) cudaFree(h->D.cand);
   if (h->h_rec) cudaFreeHost(h->h_rec);

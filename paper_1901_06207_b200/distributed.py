@@ -45,6 +45,35 @@ def exchange_owned(cube, rank: int, world: int, n_cs: int, cs_bytes: int, merge_
     return lo, hi
 
 
+class PeerExchange:
+    """The exchange without a staging collective: every rank's cube lives in torch symmetric memory,
+    so after a device-side barrier the owner's ``cbaa_merge_slice`` kernel reads the peers' slices of
+    its CS range directly over NVLink (peer loads) and ORs them into its own — one kernel for the
+    transfer and the OR.  A second barrier keeps any rank from resetting its cube for the next window
+    while a peer may still be reading it."""
+
+    def __init__(self, nbytes: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group or dist.group.WORLD
+        self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, self.group)
+        self.ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+
+    def exchange(self, cb, rank: int, world: int, n_cs: int, cs_bytes: int, stream):
+        lo, hi = owned_range(rank, world, n_cs)
+        self.hdl.barrier(channel=0)               # every router's update is complete and visible
+        peers = [p + lo * cs_bytes for k, p in enumerate(self.ptrs) if k != rank]
+        if peers and hi > lo:
+            cb.merge_slice(peers, lo, hi, stream=stream)
+        return lo, hi
+
+    def window_done(self):
+        self.hdl.barrier(channel=1)               # peers are done reading before the next reset
+
+
 def gather_hosts(hosts: np.ndarray, rank: int, world: int, group=None):
     """Collect every rank's host list on rank 0, in the output order of S:418."""
     import torch.distributed as dist

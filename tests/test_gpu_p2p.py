@@ -1,0 +1,85 @@
+"""Caller-owned cubes (cbaa_create_ext) and the symmetric-memory exchange object on one GPU.
+
+The NVLink pull-OR itself needs ≥ 2 GPUs; here we check what one GPU can: the handle works on memory
+it does not own (a torch tensor, a symmetric-memory buffer), and the peer-pointer merge path
+(cbaa_merge_slice on raw device addresses) is the same kernel the router-merge parity tests cover."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1901_06207_b200 import workload as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_create_ext_on_torch_memory(paper):
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict, cube_bytes
+    cfg = config_from_dict(paper)
+    buf = torch.full((cube_bytes(cfg),), 0xFF, dtype=torch.uint8, device="cuda")
+    cb = Cbaa(cfg, 0, cube=buf)
+    assert cb.cube_ptr() == buf.data_ptr()
+    assert not buf.any()                           # zeroed by the library
+    w = W.generate(W.C1, 8)
+    cb.reset()
+    cb.update(torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    ref, _ = O.update(paper, w.src, w.dst)
+    assert np.array_equal(buf.cpu().numpy(), ref)
+    cb.close()
+    assert np.array_equal(buf.cpu().numpy(), ref)  # caller memory survives the handle
+
+
+def test_merge_slice_from_raw_addresses(paper):
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
+    src, dst = W.random_pairs(400_000, 2)
+    a, b, g = (Cbaa(config_from_dict(paper), 0) for _ in range(3))
+    for h, sl in ((a, slice(0, 200_000)), (b, slice(200_000, None))):
+        h.reset()
+        h.update(torch.from_numpy(src[sl].view(np.int32)).cuda(), torch.from_numpy(dst[sl].view(np.int32)).cuda())
+    g.reset()
+    csb = g.nbytes // 16
+    g.merge_slice([a.cube_ptr() + 8 * csb, b.cube_ptr() + 8 * csb], 8, 16)
+    torch.cuda.synchronize()
+    ref, _ = O.update(paper, src, dst)
+    cube = g.cube().cpu().numpy()
+    assert np.array_equal(cube[8 * csb:], ref[8 * csb:]) and not cube[: 8 * csb].any()
+
+
+def test_peer_exchange_single_rank(paper):
+    import torch.distributed as dist
+    from paper_1901_06207_b200 import distributed as D
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict, cube_bytes
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        cfg = config_from_dict(paper)
+        try:
+            peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", 0))
+        except Exception as e:
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        cb = Cbaa(cfg, 0, cube=peer.buf)
+        w = W.generate(W.C1, 9)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            cb.reset(stream)
+            cb.update(torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda(),
+                      stream)
+            lo, hi = peer.exchange(cb, 0, 1, cb.n_cs, cb.nbytes // cb.n_cs, stream)
+            hosts, stats, rc = cb.detect(1024, cs_lo=lo, cs_hi=hi, stream=stream)
+            peer.window_done()
+        torch.cuda.synchronize()
+        ref, _ = O.update(paper, w.src, w.dst)
+        assert (lo, hi) == (0, 16)
+        assert np.array_equal(peer.buf.cpu().numpy(), ref)
+        st, oh, _ = O.detect(paper, ref, 1024)
+        assert hosts["ip"].tolist() == oh["ip"].tolist()
+    finally:
+        dist.destroy_process_group()
