@@ -18,6 +18,17 @@
 
 using namespace cbaa;
 
+struct DetectKey {
+  uint32_t cs_lo = 0, cs_hi = 0, theta = 0;
+  int record = 0;
+  const void* cand = nullptr;
+  const void* h_res = nullptr;
+  bool operator==(const DetectKey& o) const {
+    return cs_lo == o.cs_lo && cs_hi == o.cs_hi && theta == o.theta && record == o.record && cand == o.cand &&
+           h_res == o.h_res;
+  }
+};
+
 struct cbaa_handle {
   cbaa_config cfg;
   Geo G;
@@ -49,6 +60,10 @@ struct cbaa_handle {
   uint64_t stage_pairs = 0;
   uint64_t launches = 0;
   int upd_blocks = 0;
+  // detect graph (captured on cap_stream, launched on the caller's stream)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  DetectKey graph_key{};
   std::string err;
 };
 
@@ -447,6 +462,8 @@ void cbaa_destroy(cbaa_handle* h) {
     if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
   }
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
 }
 
@@ -576,8 +593,9 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   const Geo& G = h->G;
   uint32_t cmax = 0;
   for (uint32_t i = 0; i < G.num_ra; ++i) cmax = std::max(cmax, G.ncols[i]);
-  // columns per CTA: 8 warps × 8 columns each, fewer if the arrays are small
-  uint32_t chunk = std::min<uint32_t>(64, cmax);
+  // columns per CTA: 8 warps × 64 columns each (few fat CTAs: the per-CTA fence/atomic of the
+  // last-CTA protocol dominated with 64-column CTAs), fewer if the arrays are small
+  uint32_t chunk = std::min<uint32_t>(512, cmax);
   uint32_t n_chunks = (cmax + chunk - 1) / chunk;
   uint64_t grid = (uint64_t)n_range * G.num_ra * n_chunks;
   if (grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
@@ -609,20 +627,46 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t n_range = cs_hi - cs_lo;
   DetectScratch& D = h->D;
-  // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
-  CK(h, cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, s));
-  CK(h, cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), s));
-  int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, s);
-  if (rc) return rc;
-  const int grid = h->sms * 4;
-  if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, s>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-  else k_tuples<0><<<grid, kThreads, 0, s>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-  rc = launch_check(h, "k_tuples");
-  if (rc) return rc;
-  // one round trip in the common case: CS records + [n_hits | first kFirst hits]
+  // The whole device side of a detect — zeroing, k_zero_hot, k_tuples and the copy of the CS records
+  // and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured once per
+  // (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
   const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
-  CK(h, cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, s));
-  CK(h, cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, s));
+  const DetectKey key{cs_lo, cs_hi, theta, h->record, (const void*)D.cand, (const void*)h->h_res};
+  if (!h->graph_exec || !(h->graph_key == key)) {
+    if (h->graph_exec) {
+      cudaGraphExecDestroy(h->graph_exec);
+      h->graph_exec = nullptr;
+    }
+    if (!h->cap_stream) CK(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t c = h->cap_stream;
+    CK(h, cudaStreamBeginCapture(c, cudaStreamCaptureModeThreadLocal));
+    // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
+    cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, c);
+    cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), c);
+    int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c);
+    const int grid = h->sms * 4;
+    if (!rc) {
+      if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+      else k_tuples<0><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+      rc = launch_check(h, "k_tuples");
+    }
+    cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, c);
+    cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, c);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaStreamEndCapture(detect)");
+    e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
+    h->graph_key = key;
+    h->launches -= 2;   // counted at capture; counted again per graph launch below
+  }
+  CK(h, cudaGraphLaunch(h->graph_exec, s));
+  h->launches += 2;     // k_zero_hot + k_tuples
   CK(h, cudaStreamSynchronize(s));
   const uint64_t total = *(const unsigned long long*)h->h_res;
   const uint64_t got = std::min<uint64_t>(total, D.hit_cap);

@@ -464,13 +464,26 @@ __global__ void __launch_bounds__(kThreads) k_tuples(const __grid_constant__ Geo
       const cbaa_cs_stats* rec = D.rec + cs;
       uint64_t u = t - __ldg(D.prefix + cs_rel);
       const uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
+      if (total <= 0xffffffffull) {   // 32-bit mixed radix (the common case: tuple_cap ≤ 2^32)
+        uint32_t u32 = (uint32_t)u;
 #pragma unroll
-      for (int i = (NRA ? NRA : CBAA_MAX_RA) - 1; i >= 0; --i) {   // mixed radix, last index fastest
-        if (i < nra) {
-          uint32_t nh = __ldg(&rec->n_hot[i]);
-          uint64_t q = u / nh;
-          cols[i] = __ldg(hcs + G.ra_off[i] + (uint32_t)(u - q * nh));
-          u = q;
+        for (int i = (NRA ? NRA : CBAA_MAX_RA) - 1; i >= 0; --i) {   // last index fastest
+          if (i < nra) {
+            uint32_t nh = __ldg(&rec->n_hot[i]);
+            uint32_t q = u32 / nh;
+            cols[i] = __ldg(hcs + G.ra_off[i] + (u32 - q * nh));
+            u32 = q;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = (NRA ? NRA : CBAA_MAX_RA) - 1; i >= 0; --i) {
+          if (i < nra) {
+            uint32_t nh = __ldg(&rec->n_hot[i]);
+            uint64_t q = u / nh;
+            cols[i] = __ldg(hcs + G.ra_off[i] + (uint32_t)(u - q * nh));
+            u = q;
+          }
         }
       }
       pass = true;
