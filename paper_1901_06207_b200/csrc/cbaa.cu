@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -53,6 +54,7 @@ struct cbaa_handle {
   uint64_t h_hits_cap = 0;
   // candidate recording (debug)
   int record = 0;
+  int force_cartesian = 0;   // CBAA_FORCE_CARTESIAN=1: use k_tuples even for |RA| = 3 (A/B testing)
   // host-ingest pipeline
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
@@ -233,6 +235,8 @@ int alloc_scratch(cbaa_handle* h) {
   off += align_up(n_cs * sizeof(cbaa_cs_stats), 256);
   size_t o_prefix = off;
   off += align_up((n_cs + 1) * 8, 256);
+  size_t o_units = off;
+  off += align_up(n_cs * 8, 256);
   size_t o_zc = off;
   off += align_up(n_cs * G.ra_cols * 4, 256);
   size_t o_hc = off;
@@ -253,6 +257,7 @@ int alloc_scratch(cbaa_handle* h) {
   h->skipped = (unsigned long long*)(base + o_skipped);
   D.rec = (cbaa_cs_stats*)(base + o_rec);
   D.prefix = (unsigned long long*)(base + o_prefix);
+  D.units = (unsigned long long*)(base + o_units);
   D.zc = (uint32_t*)(base + o_zc);
   D.hc = (uint32_t*)(base + o_hc);
   D.hits = (cbaa_host*)(base + o_hits);
@@ -435,6 +440,8 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     double budget = 0.70 * (h->l2_bytes > 0 ? h->l2_bytes : (96 << 20));
     h->passes = (uint32_t)std::min<double>(8.0, std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget)));
   }
+  const char* fc = std::getenv("CBAA_FORCE_CARTESIAN");
+  h->force_cartesian = fc && fc[0] == '1';
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
   h->upd_blocks = std::max(1, occ);
@@ -589,7 +596,7 @@ int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t 
 }
 
 static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uint32_t theta, int finish,
-                           cudaStream_t s) {
+                           cudaStream_t s, int join = 0) {
   const Geo& G = h->G;
   uint32_t cmax = 0;
   for (uint32_t i = 0; i < G.num_ra; ++i) cmax = std::max(cmax, G.ncols[i]);
@@ -601,10 +608,10 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   if (grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
   if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
     k_zero_hot<true><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
-                                                         finish);
+                                                         finish, join);
   else
     k_zero_hot<false><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
-                                                          finish);
+                                                          finish, join);
   return launch_check(h, "k_zero_hot");
 }
 
@@ -643,12 +650,15 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
     cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, c);
     cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), c);
-    int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c);
+    // |RA| = 3: range join over the sorted hot lists; otherwise the Cartesian enumeration
+    const int join = h->G.num_ra == 3 && !h->force_cartesian;
+    int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c, join);
     const int grid = h->sms * 4;
     if (!rc) {
-      if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+      if (join) k_join3<<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+      else if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
       else k_tuples<0><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-      rc = launch_check(h, "k_tuples");
+      rc = launch_check(h, "k_tuples/k_join3");
     }
     cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, c);
     cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, c);

@@ -260,7 +260,8 @@ struct DetectScratch {
   unsigned long long* ztot;     // [n_cs] accumulators
   unsigned int* done;           // [n_cs] CTA arrival counters
   unsigned int* done_all;       // [1]
-  unsigned long long* prefix;   // [n_range + 1] tuple-space prefix (0 for overflowed CSs)
+  unsigned long long* prefix;   // [n_range + 1] prefix of the work units of k_tuples (0 for overflowed CSs)
+  unsigned long long* units;    // [n_cs] work units per CS: tuples (Cartesian) or |HC(0)|·|HC(1)| (join)
   unsigned long long* n_hits;   // [1]
   cbaa_host* hits;              // [hit_cap]
   uint32_t hit_cap;
@@ -300,7 +301,7 @@ template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
                                                        const __grid_constant__ DetectScratch D, uint32_t cs_lo,
                                                        uint32_t n_range, uint32_t chunk, uint32_t n_chunks,
-                                                       uint32_t theta, int finish) {
+                                                       uint32_t theta, int finish, int join) {
   __shared__ unsigned long long s_part[kWarps];
   __shared__ uint32_t s_warp[kWarps];
   __shared__ int s_last;
@@ -399,22 +400,20 @@ __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ G
   if (threadIdx.x == 0) {
     rec->tuples = prod;
     rec->overflow = prod > G.tuple_cap ? 1 : 0;
+    // work units of k_tuples for this CS: every tuple (Cartesian) or every (hc0, hc1) pair (join)
+    D.units[cs] = rec->overflow ? 0ull : (join ? (unsigned long long)rec->n_hot[0] * rec->n_hot[1] : prod);
     __threadfence();
     unsigned int old = atomicAdd(D.done_all, 1u);
     s_last = old == n_range - 1;
   }
   __syncthreads();
   if (!s_last) return;
-  // ---- last CS overall: exclusive prefix of the (capped) tuple counts over the range
+  // ---- last CS overall: exclusive prefix of the work units over the range
   __threadfence();
   const uint32_t per = (n_range + kThreads - 1) / kThreads;
   const uint32_t b0 = min(threadIdx.x * per, n_range), b1 = min(b0 + per, n_range);
   unsigned long long loc = 0;
-  for (uint32_t k = b0; k < b1; ++k) {
-    const cbaa_cs_stats* r = D.rec + cs_lo + k;
-    int ovf = __ldcg(&r->overflow);
-    loc += ovf ? 0ull : __ldcg(reinterpret_cast<const unsigned long long*>(&r->tuples));
-  }
+  for (uint32_t k = b0; k < b1; ++k) loc += __ldcg(D.units + cs_lo + k);
   __shared__ unsigned long long s_scan[kThreads];
   s_scan[threadIdx.x] = loc;
   __syncthreads();
@@ -427,10 +426,67 @@ __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ G
   unsigned long long run = s_scan[threadIdx.x] - loc;
   for (uint32_t k = b0; k < b1; ++k) {
     D.prefix[k] = run;
-    const cbaa_cs_stats* r = D.rec + cs_lo + k;
-    run += __ldcg(&r->overflow) ? 0ull : __ldcg(reinterpret_cast<const unsigned long long*>(&r->tuples));
+    run += __ldcg(D.units + cs_lo + k);
   }
   if (threadIdx.x == kThreads - 1) D.prefix[n_range] = s_scan[kThreads - 1];
+}
+
+// Union-column test of one candidate by the whole warp (Alg. 3) and its output.
+// All lanes call it with the same (cs, lp, ra_cols); lane 0 records the result.
+template <int NRA>
+__device__ __forceinline__ void union_check(const Geo& G, const uint32_t* __restrict__ cube,
+                                            const DetectScratch& D, uint32_t cs, uint32_t lp, const uint32_t* ra_cols,
+                                            int record) {
+  const int lane = threadIdx.x & 31;
+  const int nra = NRA ? NRA : (int)G.num_ra;
+  const uint32_t* csb = cube + (size_t)cs * G.cs_words;
+  const uint32_t* colp[CBAA_MAX_ARRAYS];
+#pragma unroll
+  for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i)
+    if (i < nra) colp[i] = csb + G.arr_off[i] + ((size_t)ra_cols[i] << G.wpc_log2);
+  for (uint32_t j = 0; j < G.num_va; ++j) {
+    uint32_t a = nra + j;
+    uint32_t c = mix32(lp ^ G.va_seeds[j]) & G.colmask[a];                // H_j(LP)
+    colp[a] = csb + G.arr_off[a] + ((size_t)c << G.wpc_log2);
+  }
+  uint32_t pop = 0;
+  if (NRA == 3 && G.num_va == 1) {   // paper shape: four columns held in registers
+    const uint32_t *p0 = colp[0], *p1 = colp[1], *p2 = colp[2], *p3 = colp[3];
+    for (uint32_t w = lane; w < G.wpc; w += 32)
+      pop += __popc(__ldcg(p0 + w) & __ldcg(p1 + w) & __ldcg(p2 + w) & __ldcg(p3 + w));   // UCol
+  } else {
+    for (uint32_t w = lane; w < G.wpc; w += 32) {
+      uint32_t v = 0xffffffffu;
+      for (uint32_t a = 0; a < G.narr; ++a) v &= __ldcg(colp[a] + w);     // UCol AND
+      pop += __popc(v);
+    }
+  }
+  pop = warp_sum(pop);
+  if (lane == 0) {
+    cbaa_cs_stats* rec = D.rec + cs;
+    const uint32_t z = G.g - pop;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&rec->candidates), 1ull);
+    if (record) {
+      unsigned long long k = atomicAdd(D.n_cand, 1ull);
+      if (k < D.cand_cap) D.cand[k] = ((unsigned long long)cs << 32) | lp;
+    }
+    if (z <= rec->zmax) {   // reject iff zero bits > θ_bn (Q16)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&rec->hits), 1ull);
+      unsigned long long k = atomicAdd(D.n_hits, 1ull);
+      if (k < D.hit_cap) {
+        const double g = (double)G.g;
+        double est = z == 0 ? (double)INFINITY : -g * log((double)z / (g - g * rec->eps));   // Thm. 2
+        if (est < 0.0) est = 0.0;
+        cbaa_host h;
+        h.ip = G.inv_a * (((lp << G.r) | cs) - G.mangle_b);      // unmangle
+        h.cs = cs;
+        h.lp = lp;
+        h.z = z;
+        h.estimate = est;
+        D.hits[k] = h;
+      }
+    }
+  }
 }
 
 // Alg. 3 over the whole tuple space of the range.  One lane per tuple for the CP check
@@ -504,52 +560,98 @@ __global__ void __launch_bounds__(kThreads) k_tuples(const __grid_constant__ Geo
     while (m) {
       const int srcl = __ffs(m) - 1;
       m &= m - 1;
-      const uint32_t c_rel = __shfl_sync(0xffffffffu, cs_rel, srcl);
+      const uint32_t c_cs = cs_lo + __shfl_sync(0xffffffffu, cs_rel, srcl);
       const uint32_t c_lp = __shfl_sync(0xffffffffu, lp, srcl);
-      const uint32_t cs = cs_lo + c_rel;
-      const uint32_t* csb = cube + (size_t)cs * G.cs_words;
-      const uint32_t* colp[CBAA_MAX_ARRAYS];
+      uint32_t c_cols[NRA ? NRA : CBAA_MAX_RA];
 #pragma unroll
-      for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i) {
-        uint32_t c = __shfl_sync(0xffffffffu, i < nra ? cols[i] : 0u, srcl);
-        if (i < nra) colp[i] = csb + G.arr_off[i] + ((size_t)c << G.wpc_log2);
+      for (int i = 0; i < (NRA ? NRA : CBAA_MAX_RA); ++i)
+        c_cols[i] = __shfl_sync(0xffffffffu, i < nra ? cols[i] : 0u, srcl);
+      union_check<NRA>(G, cube, D, c_cs, c_lp, c_cols, record);
+    }
+  }
+}
+
+// First index in the ascending list a[0..n) whose value is ≥ key.
+__device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Alg. 3 for |RA| = 3 as a range join.  HC(i) lists are ascending, so the hc_{i+1} whose first |CP(i)|
+// bits equal the last |CP(i)| bits of hc_i (Q19) form one contiguous run, found by binary
+// search.  One lane per (hc0, hc1) pair: CP(0) check, then the run of HC(2) matching CP(1), each checked
+// against the wrap condition CP(2) with hc0.  The candidate set is exactly the CP-passing tuples of the
+// Cartesian product (the oracle enumerates that product), but only the CP-consistent chains are visited.
+__global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+                                                    const __grid_constant__ DetectScratch D, uint32_t cs_lo,
+                                                    uint32_t n_range, int record) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long total = __ldcg(D.prefix + n_range);
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  const uint32_t Lmask = G.L == 32 ? 0xffffffffu : ((1u << G.L) - 1u);
+  for (uint64_t t0 = warp_id * 32; t0 < total; t0 += n_warps * 32) {
+    const uint64_t t = t0 + lane;
+    bool active = false;
+    uint32_t cs = 0, hc0 = 0, hc1 = 0, j = 0, jend = 0, n2 = 0;
+    const uint32_t* hc2list = nullptr;
+    if (t < total) {
+      uint32_t lo = 0, hi = n_range;   // CS of pair t: last k with prefix[k] ≤ t
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(D.prefix + mid) <= t) lo = mid;
+        else hi = mid;
       }
-      for (uint32_t j = 0; j < G.num_va; ++j) {
-        uint32_t a = nra + j;
-        uint32_t c = mix32(c_lp ^ G.va_seeds[j]) & G.colmask[a];            // H_j(LP)
-        colp[a] = csb + G.arr_off[a] + ((size_t)c << G.wpc_log2);
+      cs = cs_lo + lo;
+      const cbaa_cs_stats* rec = D.rec + cs;
+      const uint32_t n1 = __ldg(&rec->n_hot[1]);
+      n2 = __ldg(&rec->n_hot[2]);
+      const uint32_t u = (uint32_t)(t - __ldg(D.prefix + lo));
+      const uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
+      hc0 = __ldg(hcs + G.ra_off[0] + u / n1);
+      hc1 = __ldg(hcs + G.ra_off[1] + u % n1);
+      hc2list = hcs + G.ra_off[2];
+      // CP(0): low cp0 bits of hc0 == top cp0 bits of hc1
+      if ((hc0 & ((1u << G.cp[0]) - 1u)) == (hc1 >> (G.cbn[1] - G.cp[0]))) {
+        const uint32_t v = hc1 & ((1u << G.cp[1]) - 1u);     // CP(1) selects the run of HC(2)
+        const uint32_t sh = G.cbn[2] - G.cp[1];
+        j = lower_bound(hc2list, n2, v << sh);
+        jend = G.cp[1] == 0 ? n2 : lower_bound(hc2list, n2, (v + 1) << sh);
+        active = j < jend;
       }
-      uint32_t pop = 0;
-      for (uint32_t w = lane; w < G.wpc; w += 32) {
-        uint32_t v = 0xffffffffu;
-        for (uint32_t a = 0; a < G.narr; ++a) v &= __ldcg(colp[a] + w);   // UCol AND
-        pop += __popc(v);
+    }
+    while (__any_sync(0xffffffffu, active)) {
+      bool cand = false;
+      uint32_t hc2 = 0;
+      while (active && !cand) {
+        hc2 = __ldg(hc2list + j);
+        ++j;
+        active = j < jend;
+        cand = (hc2 & ((1u << G.cp[2]) - 1u)) == (hc0 >> (G.cbn[0] - G.cp[2]));   // CP(2), the wrap
       }
-      pop = warp_sum(pop);
-      if (lane == 0) {
-        cbaa_cs_stats* rec = D.rec + cs;
-        const uint32_t z = G.g - pop;
-        atomicAdd(reinterpret_cast<unsigned long long*>(&rec->candidates), 1ull);
-        if (record) {
-          unsigned long long k = atomicAdd(D.n_cand, 1ull);
-          if (k < D.cand_cap) D.cand[k] = ((unsigned long long)cs << 32) | c_lp;
+      uint32_t lp = 0;
+      if (cand) {
+        const uint32_t cols[3] = {hc0, hc1, hc2};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {   // LP = concatenation of the EPs
+          uint64_t x = (uint64_t)(cols[i] >> G.cp[i]) << (2 * G.L - G.clbs[i] - G.ep[i]);
+          lp |= (uint32_t)((x >> G.L) | x) & Lmask;
         }
-        if (z <= rec->zmax) {   // reject iff zero bits > θ_bn (Q16)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&rec->hits), 1ull);
-          unsigned long long k = atomicAdd(D.n_hits, 1ull);
-          if (k < D.hit_cap) {
-            const double g = (double)G.g;
-            double est = z == 0 ? (double)INFINITY : -g * log((double)z / (g - g * rec->eps));   // Thm. 2
-            if (est < 0.0) est = 0.0;
-            cbaa_host h;
-            h.ip = G.inv_a * (((c_lp << G.r) | cs) - G.mangle_b);      // unmangle
-            h.cs = cs;
-            h.lp = c_lp;
-            h.z = z;
-            h.estimate = est;
-            D.hits[k] = h;
-          }
-        }
+      }
+      unsigned int m = __ballot_sync(0xffffffffu, cand);
+      while (m) {
+        const int srcl = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t c_cs = __shfl_sync(0xffffffffu, cs, srcl);
+        const uint32_t c_lp = __shfl_sync(0xffffffffu, lp, srcl);
+        const uint32_t cols[3] = {__shfl_sync(0xffffffffu, hc0, srcl), __shfl_sync(0xffffffffu, hc1, srcl),
+                                  __shfl_sync(0xffffffffu, hc2, srcl)};
+        union_check<3>(G, cube, D, c_cs, c_lp, cols, record);
       }
     }
   }

@@ -346,3 +346,27 @@ def test_c2_full_size(paper):
     cb.update_host(w.src, w.dst)                 # the e2e path of bench.py, same window
     assert np.array_equal(gpu_cube(cb), ref)
     assert 550 <= len(hosts) <= 750
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_join_equals_cartesian(paper, seed, monkeypatch):
+    """|RA| = 3 detect runs the sorted-run CP join (k_join3); the Cartesian enumeration (k_tuples) must
+    give the same candidate set, hosts and stats (the oracle enumerates the full product)."""
+    spec = W.WindowSpec(n=2_000_000, n_hosts=40000, n_flows=400000, scanners=(1100, 1500, 3000, 9000))
+    w = W.generate(spec, seed)
+    out = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("CBAA_FORCE_CARTESIAN", force)
+        cb = handle(paper)
+        cb.record_candidates(True)
+        cb.reset()
+        cb.update(dev(w.src), dev(w.dst))
+        for theta in (512, 1024):
+            hosts, stats, rc = cb.detect(theta)
+            out.append((theta, hosts, stats, np.sort(cb.candidates())))
+    for (t1, h1, s1, c1), (t2, h2, s2, c2) in zip(out[:2], out[2:]):
+        assert t1 == t2 and np.array_equal(h1, h2) and s1 == s2 and np.array_equal(c1, c2)
+    ref, _ = O.update(paper, w.src, w.dst)
+    st, oh, ostats = O.detect(paper, ref, 512)
+    assert_hosts_equal(out[0][1], oh)
+    assert_stats_equal(out[0][2], ostats)
