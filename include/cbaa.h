@@ -90,7 +90,9 @@ typedef struct {
   uint32_t update_passes;              /* address-range passes of the update (0 = auto)   */
   uint32_t hit_capacity;               /* device hit buffer entries per detect (0 = 2^20)               */
   uint32_t update_mode;                /* CBAA_UPDATE_* (0 = CBAA_UPDATE_TEST_SET)         */
-  uint32_t reserved[5];
+  uint32_t join_capacity;              /* CP-chain buffer of the |RA| = 3 join (0 = 2^22); on overflow    */
+                                       /* detect redoes the window with the Cartesian enumeration          */
+  uint32_t reserved[4];
 } cbaa_config;
 
 /* One restored super host (Alg. 3 output). */

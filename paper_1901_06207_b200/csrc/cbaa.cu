@@ -24,9 +24,10 @@ struct DetectKey {
   int record = 0;
   const void* cand = nullptr;
   const void* h_res = nullptr;
+  int join = 0;
   bool operator==(const DetectKey& o) const {
     return cs_lo == o.cs_lo && cs_hi == o.cs_hi && theta == o.theta && record == o.record && cand == o.cand &&
-           h_res == o.h_res;
+           h_res == o.h_res && join == o.join;
   }
 };
 
@@ -66,6 +67,8 @@ struct cbaa_handle {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   DetectKey graph_key{};
+  int graph_kernels = 0;
+  int use_join = 0;          // |RA| = 3 and not forced Cartesian
   std::string err;
 };
 
@@ -227,6 +230,8 @@ int alloc_scratch(cbaa_handle* h) {
   off += 8;
   size_t o_ncand = off;
   off += 8;
+  size_t o_njoin = off;
+  off += 8;
   h->hdr_bytes = off;
   size_t o_skipped = off;
   off += 8;
@@ -237,6 +242,10 @@ int alloc_scratch(cbaa_handle* h) {
   off += align_up((n_cs + 1) * 8, 256);
   size_t o_units = off;
   off += align_up(n_cs * 8, 256);
+  // (cs, lp) chains of the join: 2^22 = 32 MiB by default; beyond it detect falls back (cbaa_detect_range)
+  const uint64_t join_cap = h->cfg.join_capacity ? h->cfg.join_capacity : (1ull << 22);
+  size_t o_join = off;
+  off += align_up(join_cap * 8, 256);
   size_t o_zc = off;
   off += align_up(n_cs * G.ra_cols * 4, 256);
   size_t o_hc = off;
@@ -258,6 +267,9 @@ int alloc_scratch(cbaa_handle* h) {
   D.rec = (cbaa_cs_stats*)(base + o_rec);
   D.prefix = (unsigned long long*)(base + o_prefix);
   D.units = (unsigned long long*)(base + o_units);
+  D.n_join = (unsigned long long*)(base + o_njoin);
+  D.join = (unsigned long long*)(base + o_join);
+  D.join_cap = join_cap;
   D.zc = (uint32_t*)(base + o_zc);
   D.hc = (uint32_t*)(base + o_hc);
   D.hits = (cbaa_host*)(base + o_hits);
@@ -442,6 +454,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
   }
   const char* fc = std::getenv("CBAA_FORCE_CARTESIAN");
   h->force_cartesian = fc && fc[0] == '1';
+  h->use_join = h->G.num_ra == 3 && !h->force_cartesian;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
   h->upd_blocks = std::max(1, occ);
@@ -638,7 +651,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   // and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured once per
   // (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
   const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
-  const DetectKey key{cs_lo, cs_hi, theta, h->record, (const void*)D.cand, (const void*)h->h_res};
+  const DetectKey key{cs_lo, cs_hi, theta, h->record, (const void*)D.cand, (const void*)h->h_res, h->use_join};
   if (!h->graph_exec || !(h->graph_key == key)) {
     if (h->graph_exec) {
       cudaGraphExecDestroy(h->graph_exec);
@@ -650,15 +663,24 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
     cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, c);
     cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), c);
-    // |RA| = 3: range join over the sorted hot lists; otherwise the Cartesian enumeration
-    const int join = h->G.num_ra == 3 && !h->force_cartesian;
+    // |RA| = 3: range join over the sorted hot lists, then one warp per chain; otherwise (or after a
+    // join-buffer overflow) the Cartesian enumeration with the union check inline
+    const int join = h->use_join;
     int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c, join);
     const int grid = h->sms * 4;
     if (!rc) {
-      if (join) k_join3<<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-      else if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-      else k_tuples<0><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-      rc = launch_check(h, "k_tuples/k_join3");
+      if (join) {
+        k_join3<<<grid, kThreads, 0, c>>>(h->G, D, cs_lo, n_range);
+        rc = launch_check(h, "k_join3");
+        if (!rc) {
+          k_union<<<grid, kThreads, 0, c>>>(h->G, h->cube, D, h->record);
+          rc = launch_check(h, "k_union");
+        }
+      } else {
+        if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+        else k_tuples<0><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+        rc = launch_check(h, "k_tuples");
+      }
     }
     cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, c);
     cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, c);
@@ -673,11 +695,20 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
     h->graph_key = key;
-    h->launches -= 2;   // counted at capture; counted again per graph launch below
+    h->graph_kernels = join ? 3 : 2;
+    h->launches -= h->graph_kernels;   // counted at capture; counted again per graph launch below
   }
   CK(h, cudaGraphLaunch(h->graph_exec, s));
-  h->launches += 2;     // k_zero_hot + k_tuples
+  h->launches += h->graph_kernels;
   CK(h, cudaStreamSynchronize(s));
+  if (h->use_join && ((const unsigned long long*)h->h_res)[1] > D.join_cap) {
+    // more CP chains than the join buffer holds: redo this window with the Cartesian enumeration
+    // (bounded by tuple_cap per CS, no buffer); the stats and hits are recomputed from scratch
+    h->use_join = 0;
+    int rc2 = cbaa_detect_range(h, theta, cs_lo, cs_hi, out, cap, n_out, stats, stream);
+    h->use_join = 1;
+    return rc2;
+  }
   const uint64_t total = *(const unsigned long long*)h->h_res;
   const uint64_t got = std::min<uint64_t>(total, D.hit_cap);
   if (got > kFirst) {

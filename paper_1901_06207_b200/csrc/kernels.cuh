@@ -268,6 +268,9 @@ struct DetectScratch {
   unsigned long long* n_cand;   // [1]   candidate recording (debug)
   unsigned long long* cand;     // [cand_cap]
   uint64_t cand_cap;
+  unsigned long long* n_join;   // [1]   CP-consistent chains found by k_join3 (may exceed join_cap)
+  unsigned long long* join;     // [join_cap] (cs << 32 | lp) of each chain, consumed by k_union
+  uint64_t join_cap;
 };
 
 // Block-wide exclusive prefix sum of one value per thread; returns the block total in *total.
@@ -315,7 +318,10 @@ __global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ G
   unsigned long long part = 0;
   const uint32_t* arr = cube + (size_t)cs * G.cs_words + G.arr_off[i];
   uint32_t* zc = D.zc + (size_t)cs * G.ra_cols + G.ra_off[i];
-  if (finish && blockIdx.x == 0 && threadIdx.x == 0) *D.n_hits = 0;   // k_tuples runs after this grid
+  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {   // k_tuples / k_join3 run after this grid
+    D.n_hits[0] = 0;
+    D.n_hits[1] = 0;   // result-block slot for the chain count (written by k_union)
+  }
   for (uint32_t base = c0 + warp; base < c1; base += 8 * kWarps) {
     uint32_t pop[8];
     if (VEC) {
@@ -582,23 +588,22 @@ __device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ a, 
   return lo;
 }
 
-// Alg. 3 for |RA| = 3 as a range join.  HC(i) lists are ascending, so the hc_{i+1} whose first |CP(i)|
-// bits equal the last |CP(i)| bits of hc_i (Q19) form one contiguous run, found by binary
-// search.  One lane per (hc0, hc1) pair: CP(0) check, then the run of HC(2) matching CP(1), each checked
-// against the wrap condition CP(2) with hc0.  The candidate set is exactly the CP-passing tuples of the
-// Cartesian product (the oracle enumerates that product), but only the CP-consistent chains are visited.
-__global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
-                                                    const __grid_constant__ DetectScratch D, uint32_t cs_lo,
-                                                    uint32_t n_range, int record) {
+// Alg. 3 for |RA| = 3, first half, as a range join.  HC(i) lists are ascending, so the hc_{i+1} whose
+// first |CP(i)| bits equal the last |CP(i)| bits of hc_i (Q19) form one contiguous run, found by
+// binary search.  One lane per (hc0, hc1) pair: CP(0) check, then the run of HC(2) matching CP(1), each
+// checked against the wrap condition CP(2) with hc0; every passing chain's LP is appended to
+// D.join.  The chain set is exactly the CP-passing tuples of the Cartesian product the oracle
+// enumerates, but only CP-consistent chains are visited (~n² instead of n³ work).
+__global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
+                                                    uint32_t cs_lo, uint32_t n_range) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = __ldcg(D.prefix + n_range);
-  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint32_t Lmask = G.L == 32 ? 0xffffffffu : ((1u << G.L) - 1u);
-  for (uint64_t t0 = warp_id * 32; t0 < total; t0 += n_warps * 32) {
-    const uint64_t t = t0 + lane;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); base < total; base += stride) {
+    const uint64_t t = base + lane;
     bool active = false;
-    uint32_t cs = 0, hc0 = 0, hc1 = 0, j = 0, jend = 0, n2 = 0;
+    uint32_t cs = 0, hc0 = 0, hc1 = 0, j = 0, jend = 0;
     const uint32_t* hc2list = nullptr;
     if (t < total) {
       uint32_t lo = 0, hi = n_range;   // CS of pair t: last k with prefix[k] ≤ t
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo 
       cs = cs_lo + lo;
       const cbaa_cs_stats* rec = D.rec + cs;
       const uint32_t n1 = __ldg(&rec->n_hot[1]);
-      n2 = __ldg(&rec->n_hot[2]);
+      const uint32_t n2 = __ldg(&rec->n_hot[2]);
       const uint32_t u = (uint32_t)(t - __ldg(D.prefix + lo));
       const uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
       hc0 = __ldg(hcs + G.ra_off[0] + u / n1);
@@ -625,35 +630,47 @@ __global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo 
         active = j < jend;
       }
     }
-    while (__any_sync(0xffffffffu, active)) {
-      bool cand = false;
-      uint32_t hc2 = 0;
-      while (active && !cand) {
-        hc2 = __ldg(hc2list + j);
-        ++j;
-        active = j < jend;
-        cand = (hc2 & ((1u << G.cp[2]) - 1u)) == (hc0 >> (G.cbn[0] - G.cp[2]));   // CP(2), the wrap
-      }
-      uint32_t lp = 0;
-      if (cand) {
-        const uint32_t cols[3] = {hc0, hc1, hc2};
+    // LP bits contributed by hc0 and hc1; hc2 adds its EP per chain
+    uint32_t lp01 = 0;
+    {
+      const uint32_t c01[2] = {hc0, hc1};
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {   // LP = concatenation of the EPs
-          uint64_t x = (uint64_t)(cols[i] >> G.cp[i]) << (2 * G.L - G.clbs[i] - G.ep[i]);
-          lp |= (uint32_t)((x >> G.L) | x) & Lmask;
-        }
-      }
-      unsigned int m = __ballot_sync(0xffffffffu, cand);
-      while (m) {
-        const int srcl = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t c_cs = __shfl_sync(0xffffffffu, cs, srcl);
-        const uint32_t c_lp = __shfl_sync(0xffffffffu, lp, srcl);
-        const uint32_t cols[3] = {__shfl_sync(0xffffffffu, hc0, srcl), __shfl_sync(0xffffffffu, hc1, srcl),
-                                  __shfl_sync(0xffffffffu, hc2, srcl)};
-        union_check<3>(G, cube, D, c_cs, c_lp, cols, record);
+      for (int i = 0; i < 2; ++i) {
+        uint64_t x = (uint64_t)(c01[i] >> G.cp[i]) << (2 * G.L - G.clbs[i] - G.ep[i]);
+        lp01 |= (uint32_t)((x >> G.L) | x) & Lmask;
       }
     }
+    const uint32_t top0 = hc0 >> (G.cbn[0] - G.cp[2]);
+    for (; active; ++j) {
+      active = j + 1 < jend;
+      const uint32_t hc2 = __ldg(hc2list + j);
+      if ((hc2 & ((1u << G.cp[2]) - 1u)) == top0) {                  // CP(2), the wrap
+        uint64_t x = (uint64_t)(hc2 >> G.cp[2]) << (2 * G.L - G.clbs[2] - G.ep[2]);
+        const uint32_t lp = lp01 | ((uint32_t)((x >> G.L) | x) & Lmask);
+        unsigned long long k = atomicAdd(D.n_join, 1ull);
+        if (k < D.join_cap) D.join[k] = ((unsigned long long)cs << 32) | lp;
+      }
+    }
+  }
+}
+
+// Alg. 3, second half: one warp per chain of D.join — the RA columns are the LP's own extraction
+// (Alg. 1, the round trip lpFromTuple ∘ raColumnIndex = id), the VA columns H_j(LP).
+__global__ void __launch_bounds__(kThreads) k_union(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+                                                    const __grid_constant__ DetectScratch D, int record) {
+  const unsigned long long n_all = __ldcg(D.n_join);
+  const unsigned long long n = min(n_all, (unsigned long long)D.join_cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) D.n_hits[1] = n_all;   // lets the host see a join-buffer overflow
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t k = warp_id; k < n; k += n_warps) {
+    const unsigned long long e = __ldcg(D.join + k);
+    const uint32_t cs = (uint32_t)(e >> 32), lp = (uint32_t)e;
+    const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+    uint32_t cols[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) cols[i] = (uint32_t)(dbl >> G.sh[i]) & G.colmask[i];
+    union_check<3>(G, cube, D, cs, lp, cols, record);
   }
 }
 

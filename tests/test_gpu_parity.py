@@ -370,3 +370,11 @@ def test_join_equals_cartesian(paper, seed, monkeypatch):
     st, oh, ostats = O.detect(paper, ref, 512)
     assert_hosts_equal(out[0][1], oh)
     assert_stats_equal(out[0][2], ostats)
+
+
+def test_join_buffer_overflow_falls_back(paper):
+    """More CP chains than join_capacity: the window is redone with the Cartesian enumeration and the
+    result still equals the oracle's."""
+    w = W.generate(W.C1, 4)
+    cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024, join_capacity=4)
+    assert sum(s["candidates"] for s in stats) > 4
