@@ -611,21 +611,20 @@ int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t 
 static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uint32_t theta, int finish,
                            cudaStream_t s, int join = 0) {
   const Geo& G = h->G;
-  uint32_t cmax = 0;
-  for (uint32_t i = 0; i < G.num_ra; ++i) cmax = std::max(cmax, G.ncols[i]);
-  // columns per CTA: 8 warps × 64 columns each (few fat CTAs: the per-CTA fence/atomic of the
-  // last-CTA protocol dominated with 64-column CTAs), fewer if the arrays are small
-  uint32_t chunk = std::min<uint32_t>(512, cmax);
-  uint32_t n_chunks = (cmax + chunk - 1) / chunk;
-  uint64_t grid = (uint64_t)n_range * G.num_ra * n_chunks;
-  if (grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
+  uint64_t groups = 0;
+  for (uint32_t i = 0; i < G.num_ra; ++i) groups += (G.ncols[i] + 15) / 16;
+  groups *= n_range;
+  const int grid = (int)std::min<uint64_t>((uint64_t)h->sms * 8, std::max<uint64_t>(1, (groups + 7) / 8));
   if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
-    k_zero_hot<true><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
-                                                         finish, join);
+    k_zero_counts<true><<<grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   else
-    k_zero_hot<false><<<(unsigned)grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, chunk, n_chunks, theta,
-                                                          finish, join);
-  return launch_check(h, "k_zero_hot");
+    k_zero_counts<false><<<grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
+  int rc = launch_check(h, "k_zero_counts");
+  if (rc || !finish) return rc;
+  const uint64_t hot_grid = (uint64_t)n_range * G.num_ra;
+  if (hot_grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
+  k_hot<<<(unsigned)hot_grid, kThreads, 0, s>>>(G, h->D, cs_lo, n_range, theta, join);
+  return launch_check(h, "k_hot");
 }
 
 int cbaa_zero_counts(cbaa_handle* h, uint32_t* out, cbaa_stream stream) {
@@ -695,7 +694,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
     h->graph_key = key;
-    h->graph_kernels = join ? 3 : 2;
+    h->graph_kernels = join ? 4 : 3;
     h->launches -= h->graph_kernels;   // counted at capture; counted again per graph launch below
   }
   CK(h, cudaGraphLaunch(h->graph_exec, s));

@@ -2,10 +2,12 @@
 //   k_update      Alg. 1: 128-bit streaming loads of SoA pairs, 4 REDs per pair
 //   k_zero        window reset
 //   k_or_merge    global OR merge (Q1)
-//   k_zero_hot    zero counts (Alg. 2 input) + per-CS η/ε/θ_bn
-//                 + ordered hot-column compaction (Alg. 2) + tuple-space prefix
-//   k_tuples      Alg. 3: CP-join over HC(0)×…×HC(|RA|−1), warp-cooperative
-//                 union-column AND/popcount, output with Thm. 2 estimate
+//   k_zero_counts zero counts of the RA columns (Alg. 2 input) and Ztot per CS
+//   k_hot         per-CS η/ε/θ_bn + ordered hot-column compaction (Alg. 2) + work prefix
+//   k_join3       Alg. 3 first half for |RA| = 3: CP chains by sorted-run join
+//   k_union       Alg. 3 second half: warp-cooperative union-column AND/popcount, output with the
+//                 Thm. 2 estimate
+//   k_tuples      Alg. 3 for any |RA|: Cartesian enumeration with the union check inline
 //   k_debug_map   Alg. 1 mapping only (test hook)
 #pragma once
 #include <cuda_runtime.h>
@@ -296,118 +298,132 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return before + incl - v;
 }
 
-// grid = n_range · num_ra · n_chunks CTAs of 8 warps; each warp zero-counts columns c0+warp, c0+warp+8, …
-// with up to 8 column loads in flight (VEC: one 16-B load per lane per column, g = 4096).  The last CTA
-// of each CS finishes that CS (fp64 math + ordered Alg. 2 compaction); the last CS overall writes the
-// tuple-space prefix used by k_tuples.
+// Zero counts of every RA column of CSs [cs_lo, cs_lo + n_range) (Alg. 2 input) and the per-CS
+// RA(0) totals Ztot (η source, Q12).  Persistent grid; a warp takes 16 columns of one (cs, RA i) at a
+// time and keeps all 16 column loads in flight (VEC: one 16-B load per lane per column, g = 4096).
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_zero_hot(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
-                                                       const __grid_constant__ DetectScratch D, uint32_t cs_lo,
-                                                       uint32_t n_range, uint32_t chunk, uint32_t n_chunks,
-                                                       uint32_t theta, int finish, int join) {
-  __shared__ unsigned long long s_part[kWarps];
-  __shared__ uint32_t s_warp[kWarps];
-  __shared__ int s_last;
-  __shared__ uint32_t s_zmax;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t by = blockIdx.x / n_chunks;       // (cs, RA i) of this CTA
-  const uint32_t cs = cs_lo + by / G.num_ra;
-  const uint32_t i = by % G.num_ra;
-  const uint32_t c0 = (blockIdx.x % n_chunks) * chunk;
-  const uint32_t c1 = min(c0 + chunk, G.ncols[i]);
-  unsigned long long part = 0;
-  const uint32_t* arr = cube + (size_t)cs * G.cs_words + G.arr_off[i];
-  uint32_t* zc = D.zc + (size_t)cs * G.ra_cols + G.ra_off[i];
-  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {   // k_tuples / k_join3 run after this grid
+__global__ void __launch_bounds__(kThreads) k_zero_counts(const __grid_constant__ Geo G,
+                                                          const uint32_t* __restrict__ cube,
+                                                          const __grid_constant__ DetectScratch D, uint32_t cs_lo,
+                                                          uint32_t n_range, int finish) {
+  constexpr uint32_t kGroup = 16;
+  const int lane = threadIdx.x & 31;
+  uint32_t gpc = 0;   // column groups per CS
+  for (uint32_t i = 0; i < G.num_ra; ++i) gpc += (G.ncols[i] + kGroup - 1) / kGroup;
+  const uint64_t total = (uint64_t)n_range * gpc;
+  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {   // the Alg. 3 kernels run after this graph node
     D.n_hits[0] = 0;
     D.n_hits[1] = 0;   // result-block slot for the chain count (written by k_union)
   }
-  for (uint32_t base = c0 + warp; base < c1; base += 8 * kWarps) {
-    uint32_t pop[8];
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t gi = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; gi < total; gi += n_warps) {
+    const uint32_t cs = cs_lo + (uint32_t)(gi / gpc);
+    uint32_t rem = (uint32_t)(gi % gpc), i = 0;
+    for (;; ++i) {
+      const uint32_t gi_i = (G.ncols[i] + kGroup - 1) / kGroup;
+      if (rem < gi_i) break;
+      rem -= gi_i;
+    }
+    const uint32_t c0 = rem * kGroup, c1 = min(c0 + kGroup, G.ncols[i]);
+    const uint32_t* arr = cube + (size_t)cs * G.cs_words + G.arr_off[i];
+    uint32_t pop[kGroup];
     if (VEC) {
-      uint4 v[8];
+      uint4 v[kGroup];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        uint32_t col = base + k * kWarps;
-        v[k] = col < c1 ? __ldcg(reinterpret_cast<const uint4*>(arr + ((size_t)col << G.wpc_log2)) + lane)
-                        : make_uint4(0, 0, 0, 0);
-      }
+      for (uint32_t k = 0; k < kGroup; ++k)
+        v[k] = c0 + k < c1 ? __ldcs(reinterpret_cast<const uint4*>(arr + ((size_t)(c0 + k) << G.wpc_log2)) + lane)
+                           : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pop[k] = __popc(v[k].x) + __popc(v[k].y) + __popc(v[k].z) + __popc(v[k].w);
+      for (uint32_t k = 0; k < kGroup; ++k) pop[k] = __popc(v[k].x) + __popc(v[k].y) + __popc(v[k].z) + __popc(v[k].w);
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        uint32_t col = base + k * kWarps;
+      for (uint32_t k = 0; k < kGroup; ++k) {
         pop[k] = 0;
-        if (col < c1)
-          for (uint32_t w = lane; w < G.wpc; w += 32) pop[k] += __popc(__ldcg(arr + ((size_t)col << G.wpc_log2) + w));
+        if (c0 + k < c1)
+          for (uint32_t w = lane; w < G.wpc; w += 32) pop[k] += __popc(__ldcs(arr + ((size_t)(c0 + k) << G.wpc_log2) + w));
       }
     }
+    // lane k ends up holding the population of column c0 + k (transpose-reduce of 16 warp sums)
+    uint32_t mine = 0, zsum = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t col = base + k * kWarps;
-      uint32_t z = G.g - warp_sum(pop[k]);   // zero bits of the column
-      if (lane == 0 && col < c1) {
-        zc[col] = z;
-        part += z;
-      }
+    for (uint32_t k = 0; k < kGroup; ++k) {
+      const uint32_t t = warp_sum(pop[k]);
+      if (lane == (int)k) mine = t;
+      if (c0 + k < c1) zsum += G.g - t;
     }
+    if (lane < (int)(c1 - c0)) D.zc[(size_t)cs * G.ra_cols + G.ra_off[i] + c0 + lane] = G.g - mine;
+    if (finish && i == 0 && lane == 0) atomicAdd(D.ztot + cs, (unsigned long long)zsum);
   }
-  if (!finish) return;
-  if (lane == 0) s_part[warp] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long sum = 0;
-    for (int w = 0; w < kWarps; ++w) sum += s_part[w];
-    if (i == 0 && sum) atomicAdd(D.ztot + cs, sum);
-    __threadfence();
-    unsigned int old = atomicAdd(D.done + cs, 1u);
-    s_last = old == n_chunks * G.num_ra - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  // ---- last CTA of this CS: fp64 math, then Alg. 2 in ascending column order
-  __threadfence();
+}
+
+// One CTA per (cs, RA i) of the range, after k_zero_counts: the per-CS fp64 math (every CTA of the CS
+// computes the same values; RA(0)'s CTA records them), the ordered Alg. 2 compaction of HC(i), and — in
+// the last CTA of the CS — ∏|HC(i)|, the overflow flag and the work units of the Alg. 3 kernel; the last
+// CS overall writes the prefix of those units.
+__global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
+                                                  uint32_t cs_lo, uint32_t n_range, uint32_t theta, int join) {
+  __shared__ uint32_t s_warp[kWarps];
+  __shared__ int s_last;
+  __shared__ uint32_t s_zmax;
+  const uint32_t cs = cs_lo + blockIdx.x / G.num_ra;
+  const uint32_t a = blockIdx.x % G.num_ra;
   cbaa_cs_stats* rec = D.rec + cs;
   if (threadIdx.x == 0) {
-    unsigned long long zt = __ldcg(D.ztot + cs);
-    cs_math(G, zt, theta, rec);
-    s_zmax = rec->zmax;
+    cbaa_cs_stats st;
+    cs_math(G, __ldcg(D.ztot + cs), theta, &st);
+    if (a == 0) {
+      rec->ztot = st.ztot;
+      rec->eta = st.eta;
+      rec->eps = st.eps;
+      rec->theta_bn = st.theta_bn;
+      rec->zmax = st.zmax;
+    }
+    s_zmax = st.zmax;
   }
   __syncthreads();
   const uint32_t zmax = s_zmax;
-  const uint32_t* zcs = D.zc + (size_t)cs * G.ra_cols;
-  uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
-  unsigned long long prod = 1;
+  const uint32_t* za = D.zc + (size_t)cs * G.ra_cols + G.ra_off[a];
+  uint32_t* ha = D.hc + (size_t)cs * G.ra_cols + G.ra_off[a];
   constexpr uint32_t kPer = 16;                        // columns per thread per tile, held in registers
-  for (uint32_t a = 0; a < G.num_ra; ++a) {
-    uint32_t written = 0;
-    const uint32_t* za = zcs + G.ra_off[a];
-    for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads * kPer) {
-      const uint32_t my0 = t0 + threadIdx.x * kPer;
-      uint32_t z[kPer];
+  uint32_t written = 0;
+  for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads * kPer) {
+    const uint32_t my0 = t0 + threadIdx.x * kPer;
+    uint32_t z[kPer];
 #pragma unroll
-      for (uint32_t k = 0; k < kPer; ++k) z[k] = my0 + k < G.ncols[a] ? __ldcg(za + my0 + k) : 0xffffffffu;
-      uint32_t flags = 0;
+    for (uint32_t k = 0; k < kPer; ++k) z[k] = my0 + k < G.ncols[a] ? __ldcg(za + my0 + k) : 0xffffffffu;
+    uint32_t flags = 0;
 #pragma unroll
-      for (uint32_t k = 0; k < kPer; ++k) flags |= (z[k] <= zmax ? 1u : 0u) << k;   // P:272, Q16
-      uint32_t tot;
-      uint32_t off = written + block_exclusive_scan(__popc(flags), s_warp, &tot);
-      while (flags) {
-        int k = __ffs(flags) - 1;
-        flags &= flags - 1;
-        hcs[G.ra_off[a] + off++] = my0 + k;
-      }
-      written += tot;
+    for (uint32_t k = 0; k < kPer; ++k) flags |= (z[k] <= zmax ? 1u : 0u) << k;   // P:272, Q16
+    uint32_t tot;
+    uint32_t off = written + block_exclusive_scan(__popc(flags), s_warp, &tot);
+    while (flags) {
+      int k = __ffs(flags) - 1;
+      flags &= flags - 1;
+      ha[off++] = my0 + k;
     }
-    if (threadIdx.x == 0) rec->n_hot[a] = written;
-    prod = (written != 0 && prod > ~0ull / written) ? ~0ull : prod * written;   // saturating ∏|HC(i)|
+    written += tot;
   }
   if (threadIdx.x == 0) {
+    rec->n_hot[a] = written;
+    __threadfence();
+    unsigned int old = atomicAdd(D.done + cs, 1u);
+    s_last = old == G.num_ra - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last CTA of this CS: tuple space and work units
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long prod = 1;
+    for (uint32_t i = 0; i < G.num_ra; ++i) {
+      const uint32_t n = __ldcg(&rec->n_hot[i]);
+      prod = (n != 0 && prod > ~0ull / n) ? ~0ull : prod * n;   // saturating ∏|HC(i)|
+    }
     rec->tuples = prod;
     rec->overflow = prod > G.tuple_cap ? 1 : 0;
-    // work units of k_tuples for this CS: every tuple (Cartesian) or every (hc0, hc1) pair (join)
-    D.units[cs] = rec->overflow ? 0ull : (join ? (unsigned long long)rec->n_hot[0] * rec->n_hot[1] : prod);
+    // work units of the Alg. 3 kernel: every tuple (Cartesian) or every (hc0, hc1) pair (join)
+    D.units[cs] = rec->overflow ? 0ull
+                                : (join ? (unsigned long long)__ldcg(&rec->n_hot[0]) * __ldcg(&rec->n_hot[1]) : prod);
     __threadfence();
     unsigned int old = atomicAdd(D.done_all, 1u);
     s_last = old == n_range - 1;
