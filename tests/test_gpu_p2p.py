@@ -83,3 +83,76 @@ def test_peer_exchange_single_rank(paper):
         assert hosts["ip"].tolist() == oh["ip"].tolist()
     finally:
         dist.destroy_process_group()
+
+
+def _two_rank_worker(rank, world, port, out_dir, exchange):
+    import torch.distributed as dist
+    from paper_1901_06207_b200 import distributed as D
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict, cube_bytes
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = O.default_params()
+    w = W.generate(W.WindowSpec(n=600_000, n_hosts=20000, n_flows=120000, scanners=(2000,) * 6), 21,
+                   packet_seed=100 + rank)
+    cfg = config_from_dict(p)
+    if exchange == "p2p":
+        peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", 0))
+        cb = Cbaa(cfg, 0, cube=peer.buf)
+    else:
+        peer, cb = None, Cbaa(cfg, 0)
+    stream = torch.cuda.Stream()
+    n_cs, cs_bytes = cb.n_cs, cb.nbytes // cb.n_cs
+    with torch.cuda.stream(stream):
+        cb.reset(stream)
+        cb.update(torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda(), stream)
+        if peer:
+            lo, hi = peer.exchange(cb, rank, world, n_cs, cs_bytes, stream)
+        else:   # gloo cannot move CUDA tensors: stage the cube through host memory
+            host = cb.cube().cpu()
+            def merge(peers, lo_, hi_):
+                cb.merge_slice([q.cuda() for q in peers], lo_, hi_, stream=stream)
+            lo, hi = D.exchange_owned(host, rank, world, n_cs, cs_bytes, merge)
+        hosts, stats, rc = cb.detect(1024, cs_lo=lo, cs_hi=hi, stream=stream)
+        if peer:
+            peer.window_done()
+    torch.cuda.synchronize()
+    np.save(os.path.join(out_dir, f"src{rank}.npy"), w.src)
+    np.save(os.path.join(out_dir, f"dst{rank}.npy"), w.dst)
+    np.save(os.path.join(out_dir, f"slice{rank}.npy"), cb.cube().cpu().numpy()[lo * cs_bytes: hi * cs_bytes])
+    allh = D.gather_hosts(hosts, rank, world)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "hosts.npy"), allh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "host"])
+def test_two_ranks_one_gpu(tmp_path, exchange):
+    """Two router processes sharing one B200: the symmetric-memory pull-OR (p2p) path end to end —
+    peer pointers, device barriers, merge_slice on the peer's cube — and the staged path, against the
+    oracle of the two streams together."""
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    try:
+        mp.spawn(_two_rank_worker, args=(2, port, str(tmp_path), exchange), nprocs=2, join=True)
+    except Exception as e:
+        if exchange == "p2p" and "symm" in str(e).lower():
+            pytest.skip(f"symmetric memory with two processes on one GPU unavailable: {e}")
+        raise
+    p = O.default_params()
+    src = np.concatenate([np.load(tmp_path / f"src{r}.npy") for r in range(2)])
+    dst = np.concatenate([np.load(tmp_path / f"dst{r}.npy") for r in range(2)])
+    whole, _ = O.update(p, src, dst)
+    from paper_1901_06207_b200 import distributed as D
+    cs_bytes = whole.size // 16
+    for r in range(2):
+        lo, hi = D.owned_range(r, 2, 16)
+        assert np.array_equal(np.load(tmp_path / f"slice{r}.npy"), whole[lo * cs_bytes: hi * cs_bytes])
+    st, ref, _ = O.detect(p, whole, 1024)
+    hosts = np.load(tmp_path / "hosts.npy", allow_pickle=True)
+    assert hosts["ip"].tolist() == ref["ip"].tolist()
+    assert np.allclose(hosts["estimate"], ref["estimate"], rtol=1e-12)
