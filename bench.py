@@ -41,8 +41,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
     ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
-    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
-                    help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or NVLink pull-OR over symmetric memory")
+    ap.add_argument("--exchange", choices=["nccl", "p2p", "ipc"], default="nccl",
+                    help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or the NVLink pull-OR over "
+                         "symmetric memory (p2p) / CUDA IPC mappings (ipc)")
     return ap.parse_args()
 
 
@@ -225,6 +226,8 @@ def main():
             print(f"[bench] p2p exchange unavailable ({e}); using nccl", file=sys.stderr)
             exchange = "nccl"
     cb = Cbaa(cfg, local, cube=peer.buf if peer else None)
+    if exchange == "ipc":
+        peer = D.IpcExchange(cb, rank, world)
     n_cs = cb.n_cs
     cs_bytes = cb.nbytes // n_cs
     stream = torch.cuda.Stream()
@@ -248,9 +251,11 @@ def main():
                 else:
                     lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
         hosts, stats, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream)
-        if peer:
+        if exchange == "p2p":
             with torch.cuda.stream(stream):
                 peer.window_done()
+        elif exchange == "ipc":
+            peer.window_done(stream)
         if ev:
             ev[2].record(stream)
         return D.gather_hosts(hosts, rank, world)

@@ -228,6 +228,22 @@ int cbaa_sketch_config(const void* in, uint64_t n, cbaa_config* out, char* err, 
  * Returns after the payload has been copied (the host buffer may be reused). */
 int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_stream stream);
 
+/* ------------------------------------------------------- peer cubes (CUDA IPC)
+ * For the window-end exchange between router processes without a staging
+ * collective: each process exports its cube, opens its peers' cubes (NVLink
+ * P2P mappings on a multi-GPU node; the same device also works), and
+ * cbaa_merge_slice reads the peers' CS slices directly. */
+#define CBAA_IPC_HANDLE_BYTES 64
+
+/* Writes this handle's cube IPC handle (CBAA_IPC_HANDLE_BYTES) into out.
+ * Fails with CBAA_E_ARG for cubes created by cbaa_create_ext. */
+int cbaa_ipc_export(cbaa_handle* h, void* out);
+
+/* Maps a peer process's exported cube; *dev_ptr is valid on this handle's
+ * device until cbaa_ipc_close.  The peer cube must have the same geometry. */
+int cbaa_ipc_open(cbaa_handle* h, const void* handle, void** dev_ptr);
+int cbaa_ipc_close(cbaa_handle* h, void* dev_ptr);
+
 /* ---------------------------------------------------------------- inspection */
 
 /* Device pointer and size of the cube (for NCCL exchange and parity dumps). */

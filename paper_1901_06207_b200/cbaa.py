@@ -91,6 +91,9 @@ _SIGS = {
     "cbaa_serialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
     "cbaa_sketch_config": (C.c_int, [C.c_void_p, C.c_uint64, _P(Config), C.c_char_p, C.c_uint64]),
     "cbaa_deserialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]),
+    "cbaa_ipc_export": (C.c_int, [_h, C.c_void_p]),
+    "cbaa_ipc_open": (C.c_int, [_h, C.c_void_p, _P(C.c_void_p)]),
+    "cbaa_ipc_close": (C.c_int, [_h, C.c_void_p]),
     "cbaa_kernel_launches": (C.c_uint64, [_h]),
     "cbaa_update_passes": (C.c_uint32, [_h]),
     "cbaa_strerror": (C.c_char_p, [C.c_int]),
@@ -370,6 +373,21 @@ class Cbaa:
         self._check(lib().cbaa_deserialize(self._h, a.ctypes.data_as(C.c_void_p), a.size,
                                            SKETCH_MERGE if merge else SKETCH_REPLACE, _stream(stream)),
                     "cbaa_deserialize")
+
+    # ------------------------------------------------------------ peer cubes (CUDA IPC)
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._check(lib().cbaa_ipc_export(self._h, buf), "cbaa_ipc_export")
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = C.c_void_p()
+        buf = C.create_string_buffer(bytes(handle), 64)
+        self._check(lib().cbaa_ipc_open(self._h, buf, C.byref(p)), "cbaa_ipc_open")
+        return p.value
+
+    def ipc_close(self, ptr: int):
+        self._check(lib().cbaa_ipc_close(self._h, C.c_void_p(ptr)), "cbaa_ipc_close")
 
     @property
     def kernel_launches(self) -> int:

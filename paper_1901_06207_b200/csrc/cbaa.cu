@@ -969,6 +969,35 @@ int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_
   return rc;
 }
 
+// ------------------------------------------------------------------ peer cubes (CUDA IPC)
+static_assert(sizeof(cudaIpcMemHandle_t) == CBAA_IPC_HANDLE_BYTES, "IPC handle size");
+
+int cbaa_ipc_export(cbaa_handle* h, void* out) {
+  if (!h || !out) return CBAA_E_ARG;
+  if (h->cube_external) return fail(h, CBAA_E_ARG, "cbaa_ipc_export: the cube is caller memory");
+  DeviceGuard dg(h->device);
+  cudaIpcMemHandle_t mh;
+  CK(h, cudaIpcGetMemHandle(&mh, h->cube));
+  std::memcpy(out, &mh, sizeof mh);
+  return CBAA_OK;
+}
+
+int cbaa_ipc_open(cbaa_handle* h, const void* handle, void** dev_ptr) {
+  if (!h || !handle || !dev_ptr) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaIpcMemHandle_t mh;
+  std::memcpy(&mh, handle, sizeof mh);
+  CK(h, cudaIpcOpenMemHandle(dev_ptr, mh, cudaIpcMemLazyEnablePeerAccess));
+  return CBAA_OK;
+}
+
+int cbaa_ipc_close(cbaa_handle* h, void* dev_ptr) {
+  if (!h || !dev_ptr) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  CK(h, cudaIpcCloseMemHandle(dev_ptr));
+  return CBAA_OK;
+}
+
 uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0; }
 
 uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }

@@ -74,6 +74,45 @@ class PeerExchange:
         self.hdl.barrier(channel=1)               # peers are done reading before the next reset
 
 
+class IpcExchange:
+    """The same pull-OR over CUDA IPC mappings of the peers' library-owned cubes (no torch symmetric
+    memory needed; works between processes on one device too).  Synchronisation is host-side: the
+    window's work on the stream is finished, then a process-group barrier, then the owner's merge
+    kernel reads the peers' slices; ``window_done`` fences the next reset the same way."""
+
+    def __init__(self, cb, rank: int, world: int, group=None):
+        import torch.distributed as dist
+
+        self.cb, self.rank, self.world, self.group = cb, rank, world, group
+        handles = [None] * world
+        dist.all_gather_object(handles, cb.ipc_export(), group=group)
+        self.ptrs = [None if k == rank else cb.ipc_open(hd) for k, hd in enumerate(handles)]
+
+    def exchange(self, cb, rank: int, world: int, n_cs: int, cs_bytes: int, stream):
+        import torch.distributed as dist
+
+        lo, hi = owned_range(rank, world, n_cs)
+        stream.synchronize()
+        dist.barrier(group=self.group)            # every router's update is complete
+        peers = [p + lo * cs_bytes for p in self.ptrs if p is not None]
+        if peers and hi > lo:
+            cb.merge_slice(peers, lo, hi, stream=stream)
+        return lo, hi
+
+    def window_done(self, stream=None):
+        import torch.distributed as dist
+
+        if stream is not None:
+            stream.synchronize()
+        dist.barrier(group=self.group)            # peers are done reading before the next reset
+
+    def close(self):
+        for p in self.ptrs:
+            if p is not None:
+                self.cb.ipc_close(p)
+        self.ptrs = []
+
+
 def gather_hosts(hosts: np.ndarray, rank: int, world: int, group=None):
     """Collect every rank's host list on rank 0, in the output order of S:418."""
     import torch.distributed as dist

@@ -99,6 +99,9 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
     if exchange == "p2p":
         peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", 0))
         cb = Cbaa(cfg, 0, cube=peer.buf)
+    elif exchange == "ipc":
+        cb = Cbaa(cfg, 0)
+        peer = D.IpcExchange(cb, rank, world)
     else:
         peer, cb = None, Cbaa(cfg, 0)
     stream = torch.cuda.Stream()
@@ -114,9 +117,13 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
                 cb.merge_slice([q.cuda() for q in peers], lo_, hi_, stream=stream)
             lo, hi = D.exchange_owned(host, rank, world, n_cs, cs_bytes, merge)
         hosts, stats, rc = cb.detect(1024, cs_lo=lo, cs_hi=hi, stream=stream)
-        if peer:
+        if exchange == "p2p":
             peer.window_done()
+        elif exchange == "ipc":
+            peer.window_done(stream)
     torch.cuda.synchronize()
+    if exchange == "ipc":
+        peer.close()
     np.save(os.path.join(out_dir, f"src{rank}.npy"), w.src)
     np.save(os.path.join(out_dir, f"dst{rank}.npy"), w.dst)
     np.save(os.path.join(out_dir, f"slice{rank}.npy"), cb.cube().cpu().numpy()[lo * cs_bytes: hi * cs_bytes])
@@ -127,11 +134,12 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["p2p", "host"])
+@pytest.mark.parametrize("exchange", ["ipc", "p2p", "host"])
 def test_two_ranks_one_gpu(tmp_path, exchange):
-    """Two router processes sharing one B200: the symmetric-memory pull-OR (p2p) path end to end —
-    peer pointers, device barriers, merge_slice on the peer's cube — and the staged path, against the
-    oracle of the two streams together."""
+    """Two router processes sharing one B200: the pull-OR over CUDA IPC mappings of the peer's cube (ipc)
+    end to end — handle exchange, barriers, merge_slice reading the peer's memory — the staged path
+    (host), and the symmetric-memory variant (p2p; torch refuses two ranks on one device, so it skips),
+    each against the oracle of the two streams together."""
     import torch.multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
