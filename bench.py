@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
     ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
-    ap.add_argument("--exchange", choices=["nccl", "p2p", "ipc"], default="nccl",
+    ap.add_argument("--exchange", choices=["nccl", "p2p", "ipc"], default="ipc",
                     help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or the NVLink pull-OR over "
                          "symmetric memory (p2p) / CUDA IPC mappings (ipc)")
     return ap.parse_args()
@@ -193,6 +193,16 @@ def cpu_baseline(w, seconds_budget=20.0):
 
 
 # --------------------------------------------------------------------------------------- our arm
+def _allreduce(v: float, op) -> float:
+    """Scalar all-reduce (max over ranks for times) on the process group's own device kind."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -205,8 +215,12 @@ def main():
     from paper_1901_06207_b200.cbaa import Cbaa, default_config
 
     rank, world, local = dist_env()
+    # one GPU per rank; more ranks than GPUs (functional runs on a 1-GPU box) wrap around and then
+    # need CBAA_BENCH_BACKEND=gloo, since NCCL refuses two ranks on one device
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CBAA_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
     torch.cuda.set_device(local)
     peaks_acc = access_peaks() if rank == 0 else {}
     spec, w = workload(args.workload, args.seed, rank, world)
@@ -227,7 +241,17 @@ def main():
             exchange = "nccl"
     cb = Cbaa(cfg, local, cube=peer.buf if peer else None)
     if exchange == "ipc":
-        peer = D.IpcExchange(cb, rank, world)
+        # collective fallback: every rank must be able to map every peer cube, else all use NCCL
+        err = None
+        try:
+            peer = D.IpcExchange(cb, rank, world)
+        except Exception as e:
+            err, peer = e, None
+        if not int(_allreduce(0.0 if err else 1.0, dist.ReduceOp.MIN)):
+            if peer:
+                peer.close()
+            peer, exchange = None, "nccl"
+            print(f"[bench] ipc exchange unavailable ({err}); using nccl", file=sys.stderr)
     n_cs = cb.n_cs
     cs_bytes = cb.nbytes // n_cs
     stream = torch.cuda.Stream()
@@ -283,9 +307,7 @@ def main():
     upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
     post_ms = [e[1].elapsed_time(e[2]) for e in evs]
     if world > 1:
-        t = torch.tensor([elapsed_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+        elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
 
     # window-end detect latency alone: update finished, then detect until the host list is filled
     det_ms = []
@@ -318,9 +340,7 @@ def main():
             torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / ke
         if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = _allreduce(e2e_ms, dist.ReduceOp.MAX)
         e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 24 * nh + 104 * n_cs + 8,
                "path": "cbaa_update_host (pinned, double-buffered chunks) + cbaa_detect"}
