@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads) k_zero_counts(const __grid_constant_
 __global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
                                                   uint32_t cs_lo, uint32_t n_range, uint32_t theta, int join) {
   __shared__ uint32_t s_warp[kWarps];
-  __shared__ int s_last;
+  __shared__ int s_last, s_last_all;
   __shared__ uint32_t s_zmax;
   const uint32_t cs = cs_lo + blockIdx.x / G.num_ra;
   const uint32_t a = blockIdx.x % G.num_ra;
@@ -426,10 +426,10 @@ __global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G,
                                 : (join ? (unsigned long long)__ldcg(&rec->n_hot[0]) * __ldcg(&rec->n_hot[1]) : prod);
     __threadfence();
     unsigned int old = atomicAdd(D.done_all, 1u);
-    s_last = old == n_range - 1;
+    s_last_all = old == n_range - 1;   // a second flag: other warps may still be reading s_last
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last_all) return;
   // ---- last CS overall: exclusive prefix of the work units over the range
   __threadfence();
   const uint32_t per = (n_range + kThreads - 1) / kThreads;
