@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
     ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="N=1: run windows strictly one after another (default: window k's detect overlaps "
+                         "window k+1's reset+update on a second cube and a high-priority stream)")
     ap.add_argument("--exchange", choices=["nccl", "p2p", "ipc"], default="ipc",
                     help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or the NVLink pull-OR over "
                          "symmetric memory (p2p) / CUDA IPC mappings (ipc)")
@@ -308,6 +311,54 @@ def main():
     post_ms = [e[1].elapsed_time(e[2]) for e in evs]
     if world > 1:
         elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
+    serial_ms = elapsed_ms
+
+    # Pipelined windows (N = 1): two cubes; window k's reset+update run on the update stream while
+    # window k-1's detect runs on a high-priority stream (its 128-thread CTAs fit beside the persistent
+    # update CTAs).  Cube k%2 is reset only after the detect of window k-2 has returned (host order).
+    pipelined = world == 1 and not args.no_pipeline
+    if pipelined:
+        cb2 = Cbaa(cfg, local)
+        cbs = [cb, cb2]
+        lo_pri, hi_pri = torch.cuda.Stream.priority_range()
+        s_upd, s_det = stream, torch.cuda.Stream(priority=hi_pri)
+
+        def run_pipelined(n_win, upd_evs=None):
+            pending, out = None, None
+            for k in range(n_win):
+                c = cbs[k % 2]
+                c.reset(s_upd)
+                if upd_evs:
+                    upd_evs[k][0].record(s_upd)
+                c.update(src, dst, s_upd)
+                done = torch.cuda.Event()
+                done.record(s_upd)
+                if upd_evs:
+                    upd_evs[k][1].record(s_upd)
+                if pending:
+                    pc, pe = pending
+                    s_det.wait_event(pe)
+                    out, _, _ = pc.detect(THETA, stream=s_det)
+                pending = (c, done)
+            pc, pe = pending
+            s_det.wait_event(pe)
+            out, _, _ = pc.detect(THETA, stream=s_det)
+            return out
+
+        run_pipelined(max(args.warmup, 3))
+        torch.cuda.synchronize()
+        launches0 = cb.kernel_launches + cb2.kernel_launches
+        pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            p_start.record(s_upd)
+            hosts = run_pipelined(args.steps, pevs)
+            p_end.record(s_det)
+            torch.cuda.synchronize()
+        launches = cb.kernel_launches + cb2.kernel_launches - launches0
+        elapsed_ms = p_start.elapsed_time(p_end)
+        upd_ms = [e[0].elapsed_time(e[1]) for e in pevs]
 
     # window-end detect latency alone: update finished, then detect until the host list is filled
     det_ms = []
@@ -380,6 +431,8 @@ def main():
             "config": dict(config_block(args.workload, spec, world), exchange=exchange),
             "detect_ms": statistics.median(det_ms), "update_ms": upd,
             "post_update_ms": statistics.median(post_ms),
+            "windows": "pipelined: detect(k) overlaps reset+update(k+1), two cubes" if pipelined else "serial",
+            "ms_per_step_serial": serial_ms / args.steps,
             "update_pairs_per_s": n * world / (upd / 1e3),
             "n_super_hosts": int(len(hosts)) if hosts is not None else None,
             "roofline": roofline, "roofline_hbm": roofline_hbm,

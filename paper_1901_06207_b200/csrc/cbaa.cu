@@ -614,16 +614,17 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   uint64_t groups = 0;
   for (uint32_t i = 0; i < G.num_ra; ++i) groups += (G.ncols[i] + 15) / 16;
   groups *= n_range;
-  const int grid = (int)std::min<uint64_t>((uint64_t)h->sms * 8, std::max<uint64_t>(1, (groups + 7) / 8));
+  const int grid =
+      (int)std::min<uint64_t>((uint64_t)h->sms * 16, std::max<uint64_t>(1, (groups + kDetWarps - 1) / kDetWarps));
   if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
-    k_zero_counts<true><<<grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
+    k_zero_counts<true><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   else
-    k_zero_counts<false><<<grid, kThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
+    k_zero_counts<false><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   int rc = launch_check(h, "k_zero_counts");
   if (rc || !finish) return rc;
   const uint64_t hot_grid = (uint64_t)n_range * G.num_ra;
   if (hot_grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
-  k_hot<<<(unsigned)hot_grid, kThreads, 0, s>>>(G, h->D, cs_lo, n_range, theta, join);
+  k_hot<<<(unsigned)hot_grid, kDetThreads, 0, s>>>(G, h->D, cs_lo, n_range, theta, join);
   return launch_check(h, "k_hot");
 }
 
@@ -666,18 +667,18 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     // join-buffer overflow) the Cartesian enumeration with the union check inline
     const int join = h->use_join;
     int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c, join);
-    const int grid = h->sms * 4;
+    const int grid = h->sms * 8;
     if (!rc) {
       if (join) {
-        k_join3<<<grid, kThreads, 0, c>>>(h->G, D, cs_lo, n_range);
+        k_join3<<<grid, kDetThreads, 0, c>>>(h->G, D, cs_lo, n_range);
         rc = launch_check(h, "k_join3");
         if (!rc) {
-          k_union<<<grid, kThreads, 0, c>>>(h->G, h->cube, D, h->record);
+          k_union<<<grid, kDetThreads, 0, c>>>(h->G, h->cube, D, h->record);
           rc = launch_check(h, "k_union");
         }
       } else {
-        if (h->G.num_ra == 3) k_tuples<3><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
-        else k_tuples<0><<<grid, kThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+        if (h->G.num_ra == 3) k_tuples<3><<<grid, kDetThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
+        else k_tuples<0><<<grid, kDetThreads, 0, c>>>(h->G, h->cube, D, cs_lo, n_range, h->record);
         rc = launch_check(h, "k_tuples");
       }
     }

@@ -20,6 +20,10 @@ namespace cbaa {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+// Window-end kernels run 128-thread CTAs so that, when windows are pipelined, a detect CTA fits in the
+// registers the two persistent update CTAs leave free on every SM (2 × 8 warps × 112 regs of 64 K).
+constexpr int kDetThreads = 128;
+constexpr int kDetWarps = kDetThreads / 32;
 
 // ---------------------------------------------------------------- primitives
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
@@ -288,7 +292,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   __syncthreads();
   uint32_t before = 0, tot = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
+  for (int w = 0; w < kDetWarps; ++w) {
     uint32_t c = s_warp[w];
     before += w < warp ? c : 0u;
     tot += c;
@@ -302,7 +306,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // RA(0) totals Ztot (η source, Q12).  Persistent grid; a warp takes 16 columns of one (cs, RA i) at a
 // time and keeps all 16 column loads in flight (VEC: one 16-B load per lane per column, g = 4096).
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_zero_counts(const __grid_constant__ Geo G,
+__global__ void __launch_bounds__(kDetThreads) k_zero_counts(const __grid_constant__ Geo G,
                                                           const uint32_t* __restrict__ cube,
                                                           const __grid_constant__ DetectScratch D, uint32_t cs_lo,
                                                           uint32_t n_range, int finish) {
@@ -315,8 +319,8 @@ __global__ void __launch_bounds__(kThreads) k_zero_counts(const __grid_constant_
     D.n_hits[0] = 0;
     D.n_hits[1] = 0;   // result-block slot for the chain count (written by k_union)
   }
-  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  for (uint64_t gi = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; gi < total; gi += n_warps) {
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kDetThreads) >> 5;
+  for (uint64_t gi = ((uint64_t)blockIdx.x * kDetThreads + threadIdx.x) >> 5; gi < total; gi += n_warps) {
     const uint32_t cs = cs_lo + (uint32_t)(gi / gpc);
     uint32_t rem = (uint32_t)(gi % gpc), i = 0;
     for (;; ++i) {
@@ -360,9 +364,9 @@ __global__ void __launch_bounds__(kThreads) k_zero_counts(const __grid_constant_
 // computes the same values; RA(0)'s CTA records them), the ordered Alg. 2 compaction of HC(i), and — in
 // the last CTA of the CS — ∏|HC(i)|, the overflow flag and the work units of the Alg. 3 kernel; the last
 // CS overall writes the prefix of those units.
-__global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
+__global__ void __launch_bounds__(kDetThreads) k_hot(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
                                                   uint32_t cs_lo, uint32_t n_range, uint32_t theta, int join) {
-  __shared__ uint32_t s_warp[kWarps];
+  __shared__ uint32_t s_warp[kDetWarps];
   __shared__ int s_last, s_last_all;
   __shared__ uint32_t s_zmax;
   const uint32_t cs = cs_lo + blockIdx.x / G.num_ra;
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G,
   uint32_t* ha = D.hc + (size_t)cs * G.ra_cols + G.ra_off[a];
   constexpr uint32_t kPer = 16;                        // columns per thread per tile, held in registers
   uint32_t written = 0;
-  for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kThreads * kPer) {
+  for (uint32_t t0 = 0; t0 < G.ncols[a]; t0 += kDetThreads * kPer) {
     const uint32_t my0 = t0 + threadIdx.x * kPer;
     uint32_t z[kPer];
 #pragma unroll
@@ -432,14 +436,14 @@ __global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G,
   if (!s_last_all) return;
   // ---- last CS overall: exclusive prefix of the work units over the range
   __threadfence();
-  const uint32_t per = (n_range + kThreads - 1) / kThreads;
+  const uint32_t per = (n_range + kDetThreads - 1) / kDetThreads;
   const uint32_t b0 = min(threadIdx.x * per, n_range), b1 = min(b0 + per, n_range);
   unsigned long long loc = 0;
   for (uint32_t k = b0; k < b1; ++k) loc += __ldcg(D.units + cs_lo + k);
-  __shared__ unsigned long long s_scan[kThreads];
+  __shared__ unsigned long long s_scan[kDetThreads];
   s_scan[threadIdx.x] = loc;
   __syncthreads();
-  for (int o = 1; o < kThreads; o <<= 1) {   // Hillis-Steele inclusive scan
+  for (int o = 1; o < kDetThreads; o <<= 1) {   // Hillis-Steele inclusive scan
     unsigned long long v = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0ull;
     __syncthreads();
     s_scan[threadIdx.x] += v;
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) k_hot(const __grid_constant__ Geo G,
     D.prefix[k] = run;
     run += __ldcg(D.units + cs_lo + k);
   }
-  if (threadIdx.x == kThreads - 1) D.prefix[n_range] = s_scan[kThreads - 1];
+  if (threadIdx.x == kDetThreads - 1) D.prefix[n_range] = s_scan[kDetThreads - 1];
 }
 
 // Union-column test of one candidate by the whole warp (Alg. 3) and its output.
@@ -515,14 +519,14 @@ __device__ __forceinline__ void union_check(const Geo& G, const uint32_t* __rest
 // and LP assembly; passing tuples are then checked one at a time by the
 // whole warp: AND of the |RA|+|VA| columns, popcount, Z ≤ zmax.
 template <int NRA>
-__global__ void __launch_bounds__(kThreads) k_tuples(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+__global__ void __launch_bounds__(kDetThreads) k_tuples(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
                                                      const __grid_constant__ DetectScratch D, uint32_t cs_lo,
                                                      uint32_t n_range, int record) {
   const int lane = threadIdx.x & 31;
   const int nra = NRA ? NRA : (int)G.num_ra;
   const unsigned long long total = __ldcg(D.prefix + n_range);
-  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * kDetThreads + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kDetThreads) >> 5;
   const uint32_t Lmask = G.L == 32 ? 0xffffffffu : ((1u << G.L) - 1u);
   for (uint64_t t0 = warp_id * 32; t0 < total; t0 += n_warps * 32) {
     const uint64_t t = t0 + lane;
@@ -610,13 +614,13 @@ __device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ a, 
 // checked against the wrap condition CP(2) with hc0; every passing chain's LP is appended to
 // D.join.  The chain set is exactly the CP-passing tuples of the Cartesian product the oracle
 // enumerates, but only CP-consistent chains are visited (~n² instead of n³ work).
-__global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
+__global__ void __launch_bounds__(kDetThreads) k_join3(const __grid_constant__ Geo G, const __grid_constant__ DetectScratch D,
                                                     uint32_t cs_lo, uint32_t n_range) {
   const int lane = threadIdx.x & 31;
   const unsigned long long total = __ldcg(D.prefix + n_range);
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t stride = (uint64_t)gridDim.x * kDetThreads;
   const uint32_t Lmask = G.L == 32 ? 0xffffffffu : ((1u << G.L) - 1u);
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); base < total; base += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * kDetThreads + (threadIdx.x & ~31u); base < total; base += stride) {
     const uint64_t t = base + lane;
     bool active = false;
     uint32_t cs = 0, hc0 = 0, hc1 = 0, j = 0, jend = 0;
@@ -672,13 +676,13 @@ __global__ void __launch_bounds__(kThreads) k_join3(const __grid_constant__ Geo 
 
 // Alg. 3, second half: one warp per chain of D.join — the RA columns are the LP's own extraction
 // (Alg. 1, the round trip lpFromTuple ∘ raColumnIndex = id), the VA columns H_j(LP).
-__global__ void __launch_bounds__(kThreads) k_union(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
+__global__ void __launch_bounds__(kDetThreads) k_union(const __grid_constant__ Geo G, const uint32_t* __restrict__ cube,
                                                     const __grid_constant__ DetectScratch D, int record) {
   const unsigned long long n_all = __ldcg(D.n_join);
   const unsigned long long n = min(n_all, (unsigned long long)D.join_cap);
   if (blockIdx.x == 0 && threadIdx.x == 0) D.n_hits[1] = n_all;   // lets the host see a join-buffer overflow
-  const uint64_t warp_id = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * kDetThreads + threadIdx.x) >> 5;
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kDetThreads) >> 5;
   for (uint64_t k = warp_id; k < n; k += n_warps) {
     const unsigned long long e = __ldcg(D.join + k);
     const uint32_t cs = (uint32_t)(e >> 32), lp = (uint32_t)e;
