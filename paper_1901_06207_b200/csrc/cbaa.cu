@@ -526,14 +526,13 @@ int cbaa_update_host(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, u
     for (int b = 0; b < 2; ++b) {
       CK(h, cudaEventCreateWithFlags(&h->ev_copied[b], cudaEventDisableTiming));
       CK(h, cudaEventCreateWithFlags(&h->ev_free[b], cudaEventDisableTiming));
+      CK(h, cudaEventRecord(h->ev_free[b], h->copy_stream));   // both staging buffers start free
       for (int a = 0; a < 2; ++a) CK(h, cudaMalloc(&h->stage[b][a], chunk * 4));
     }
     h->stage_pairs = chunk;
   }
-  // the copy stream may not start before earlier work on `s` that still reads the staging buffers
-  for (int b = 0; b < 2; ++b) {
-    CK(h, cudaEventRecord(h->ev_free[b], s));
-  }
+  // ev_free[b] always marks the end of the last update that read staging buffer b — on whatever
+  // stream that call used — so a copy into b waits for it even across calls on different streams
   uint64_t k = 0;
   for (uint64_t off = 0; off < n; off += h->stage_pairs, ++k) {
     const int b = (int)(k & 1);
