@@ -378,3 +378,46 @@ def test_join_buffer_overflow_falls_back(paper):
     w = W.generate(W.C1, 4)
     cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024, join_capacity=4)
     assert sum(s["candidates"] for s in stats) > 4
+
+
+def test_update_host_across_streams(paper):
+    """Consecutive host-ingest calls on different streams reuse the staging buffers safely."""
+    src, dst = W.random_pairs(18_000_000, 17)
+    cb = handle(paper)
+    cb.reset()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    cut = 9_000_001
+    cb.update_host(src[:cut], dst[:cut], stream=s1)
+    s2.wait_stream(s1)
+    cb.update_host(src[cut:], dst[cut:], stream=s2)
+    torch.cuda.synchronize()
+    ref, _ = O.update(paper, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+def test_pipelined_windows(paper):
+    """bench.py's pipelined schedule (two cubes; detect of window k on a high-priority stream while
+    window k+1 resets and updates) returns each window's own super hosts."""
+    wins = [W.generate(W.WindowSpec(n=400_000, n_hosts=10_000, n_flows=60_000, scanners=(2000,) * 3), 30 + k)
+            for k in range(5)]
+    cbs = [handle(paper), handle(paper)]
+    s_upd = torch.cuda.Stream()
+    s_det = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
+    got, pending = [], None
+    for k, w in enumerate(wins):
+        c = cbs[k % 2]
+        c.reset(s_upd)
+        c.update(dev(w.src), dev(w.dst), s_upd)
+        done = torch.cuda.Event()
+        done.record(s_upd)
+        if pending:
+            s_det.wait_event(pending[1])
+            got.append(pending[0].detect(1024, stream=s_det)[0])
+        pending = (c, done)
+    s_det.wait_event(pending[1])
+    got.append(pending[0].detect(1024, stream=s_det)[0])
+    for w, h in zip(wins, got):
+        ref, _ = O.update(paper, w.src, w.dst)
+        st, oh, _ = O.detect(paper, ref, 1024)
+        assert_hosts_equal(h, oh)
+        assert set(w.planted) <= set(h["ip"].tolist())
