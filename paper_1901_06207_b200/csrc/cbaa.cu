@@ -56,6 +56,7 @@ struct cbaa_handle {
   // candidate recording (debug)
   int record = 0;
   int force_cartesian = 0;   // CBAA_FORCE_CARTESIAN=1: use k_tuples even for |RA| = 3 (A/B testing)
+  int no_tma = 0;            // CBAA_NO_TMA=1: register-load zero counts instead of the TMA pipeline (A/B)
   // host-ingest pipeline
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
@@ -455,6 +456,8 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
   const char* fc = std::getenv("CBAA_FORCE_CARTESIAN");
   h->force_cartesian = fc && fc[0] == '1';
   h->use_join = h->G.num_ra == 3 && !h->force_cartesian;
+  const char* nt = std::getenv("CBAA_NO_TMA");
+  h->no_tma = nt && nt[0] == '1';
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
   h->upd_blocks = std::max(1, occ);
@@ -615,7 +618,12 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   groups *= n_range;
   const int grid =
       (int)std::min<uint64_t>((uint64_t)h->sms * 16, std::max<uint64_t>(1, (groups + kDetWarps - 1) / kDetWarps));
-  if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
+  // g = 4096 with RA blocks of whole 16-column tiles (every c(i) ≥ 16): TMA-streamed zero counts
+  bool tma = G.wpc == 128 && !h->no_tma;
+  for (uint32_t i = 0; i < G.num_ra; ++i) tma = tma && G.ncols[i] % kZcTileCols == 0;
+  if (tma)
+    k_zero_counts_tma<<<h->sms * 4, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
+  else if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
     k_zero_counts<true><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   else
     k_zero_counts<false><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);

@@ -302,6 +302,85 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return before + incl - v;
 }
 
+// ---------------------------------------------------------------- TMA bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_addr(b)), "r"(parity) : "memory");
+  }
+}
+// 1-D bulk copy global → shared (TMA engine), completion counted on the mbarrier; bytes % 16 == 0.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(0x12F0000000000000ull)   // evict_first
+               : "memory");
+}
+
+// Zero counts for g = 4096 (a column = 512 B) streamed by the TMA engine: the RA block of a CS is
+// contiguous, so it is cut into 8 KiB tiles of 16 columns; persistent CTAs run a kStages-deep
+// cp.async.bulk + mbarrier pipeline and each warp popcounts 4 columns of a tile out of shared memory.
+// The copies need no registers, so far more bytes are in flight than with register loads.
+constexpr int kZcStages = 4;
+constexpr uint32_t kZcTileCols = 16;
+__global__ void __launch_bounds__(kDetThreads) k_zero_counts_tma(const __grid_constant__ Geo G,
+                                                                 const uint32_t* __restrict__ cube,
+                                                                 const __grid_constant__ DetectScratch D,
+                                                                 uint32_t cs_lo, uint32_t n_range, int finish) {
+  __shared__ __align__(128) uint4 tile[kZcStages][kZcTileCols * 32];   // 16 columns × 512 B per stage
+  __shared__ __align__(8) uint64_t bar[kZcStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t tiles_per_cs = G.ra_cols / kZcTileCols;
+  const uint64_t n_tiles = (uint64_t)n_range * tiles_per_cs;
+  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {
+    D.n_hits[0] = 0;
+    D.n_hits[1] = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kZcStages; ++k) mbar_init(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](uint64_t t, int st) {
+    const uint32_t cs = cs_lo + (uint32_t)(t / tiles_per_cs);
+    const uint32_t col0 = (uint32_t)(t % tiles_per_cs) * kZcTileCols;   // column index within the RA block
+    const uint32_t* src = cube + (size_t)cs * G.cs_words + ((size_t)col0 << G.wpc_log2);
+    mbar_expect_tx(&bar[st], kZcTileCols * 512);
+    bulk_load(tile[st], src, kZcTileCols * 512, &bar[st]);
+  };
+  uint64_t t = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kZcStages; ++k)
+      if (t + (uint64_t)k * gridDim.x < n_tiles) issue(t + (uint64_t)k * gridDim.x, k);
+  for (uint32_t it = 0; t < n_tiles; t += gridDim.x, ++it) {
+    const int st = it % kZcStages;
+    mbar_wait(&bar[st], (it / kZcStages) & 1);
+    const uint32_t cs = cs_lo + (uint32_t)(t / tiles_per_cs);
+    const uint32_t col0 = (uint32_t)(t % tiles_per_cs) * kZcTileCols;
+    uint32_t zsum = 0;
+#pragma unroll
+    for (int k = 0; k < (int)kZcTileCols / kDetWarps; ++k) {
+      const uint32_t c = warp * (kZcTileCols / kDetWarps) + k;
+      const uint4 v = tile[st][c * 32 + lane];
+      const uint32_t pop = warp_sum(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w));
+      const uint32_t z = G.g - pop;                                      // zero bits
+      if (lane == 0) D.zc[(size_t)cs * G.ra_cols + col0 + c] = z;
+      zsum += z;
+    }
+    __syncthreads();   // the whole tile has been read: refill this stage
+    if (threadIdx.x == 0 && t + (uint64_t)kZcStages * gridDim.x < n_tiles) issue(t + (uint64_t)kZcStages * gridDim.x, st);
+    // RA(0) columns are the first c(0) of the block: Ztot (Q12)
+    if (finish && lane == 0 && col0 < G.ncols[0]) atomicAdd(D.ztot + cs, (unsigned long long)zsum);
+  }
+}
+
 // Zero counts of every RA column of CSs [cs_lo, cs_lo + n_range) (Alg. 2 input) and the per-CS
 // RA(0) totals Ztot (η source, Q12).  Persistent grid; a warp takes 16 columns of one (cs, RA i) at a
 // time and keeps all 16 column loads in flight (VEC: one 16-B load per lane per column, g = 4096).

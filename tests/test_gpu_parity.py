@@ -421,3 +421,19 @@ def test_pipelined_windows(paper):
         st, oh, _ = O.detect(paper, ref, 1024)
         assert_hosts_equal(h, oh)
         assert set(w.planted) <= set(h["ip"].tolist())
+
+
+@pytest.mark.parametrize("no_tma", ["0", "1"])
+def test_zero_count_paths(paper, no_tma, monkeypatch):
+    """The TMA-streamed zero counts (g = 4096) and the register-load kernel give the oracle's counts."""
+    monkeypatch.setenv("CBAA_NO_TMA", no_tma)
+    w = W.generate(W.C1, 6)
+    cb = handle(paper)
+    cb.reset()
+    cb.update(dev(w.src), dev(w.dst))
+    ref, _ = O.update(paper, w.src, w.dst)
+    assert np.array_equal(cb.zero_counts().cpu().numpy().view(np.uint32), O.zero_counts_ra(paper, ref))
+    hosts, stats, rc = cb.detect(1024)
+    st, oh, ostats = O.detect(paper, ref, 1024)
+    assert_stats_equal(stats, ostats)
+    assert_hosts_equal(hosts, oh)
