@@ -92,7 +92,10 @@ typedef struct {
   uint32_t update_mode;                /* CBAA_UPDATE_* (0 = CBAA_UPDATE_TEST_SET)         */
   uint32_t join_capacity;              /* CP-chain buffer of the |RA| = 3 join (0 = 2^22); on overflow    */
                                        /* detect redoes the window with the Cartesian enumeration          */
-  uint32_t reserved[4];
+  uint32_t detect_overlap;             /* 1: detect will run beside another handle's update (pipelined    */
+                                       /* windows): window-end kernels use no shared memory so they fit   */
+                                       /* next to the update's CTAs; 0: fastest standalone detect (TMA)   */
+  uint32_t reserved[3];
 } cbaa_config;
 
 /* One restored super host (Alg. 3 output). */

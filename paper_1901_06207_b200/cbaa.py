@@ -35,7 +35,8 @@ class Config(C.Structure):
         ("theta_formula", C.c_int32), ("direction", C.c_int32), ("tuple_cap", C.c_uint64),
         ("n_prefixes", C.c_uint32), ("inner_prefix", C.c_uint32 * MAX_PREFIXES),
         ("inner_mask", C.c_uint32 * MAX_PREFIXES), ("update_passes", C.c_uint32), ("hit_capacity", C.c_uint32),
-        ("update_mode", C.c_uint32), ("join_capacity", C.c_uint32), ("reserved", C.c_uint32 * 4),
+        ("update_mode", C.c_uint32), ("join_capacity", C.c_uint32), ("detect_overlap", C.c_uint32),
+        ("reserved", C.c_uint32 * 3),
     ]
 
     def to_dict(self) -> dict:
@@ -151,6 +152,7 @@ def config_from_dict(p: dict) -> Config:
     c.hit_capacity = p.get("hit_capacity", 0)
     c.update_mode = p.get("update_mode", UPDATE_TEST_SET)
     c.join_capacity = p.get("join_capacity", 0)
+    c.detect_overlap = p.get("detect_overlap", 0)
     return c
 
 

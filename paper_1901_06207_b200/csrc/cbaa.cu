@@ -619,7 +619,7 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   const int grid =
       (int)std::min<uint64_t>((uint64_t)h->sms * 16, std::max<uint64_t>(1, (groups + kDetWarps - 1) / kDetWarps));
   // g = 4096 with RA blocks of whole 16-column tiles (every c(i) ≥ 16): TMA-streamed zero counts
-  bool tma = G.wpc == 128 && !h->no_tma;
+  bool tma = G.wpc == 128 && !h->no_tma && !h->cfg.detect_overlap;
   for (uint32_t i = 0; i < G.num_ra; ++i) tma = tma && G.ncols[i] % kZcTileCols == 0;
   if (tma)
     k_zero_counts_tma<<<h->sms * 4, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
