@@ -161,6 +161,11 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
  * accepted (16-B aligned arrays take the vector path).  Async on stream. */
 int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream);
 
+/* Same for interleaved ("packed") pairs in one DEVICE array: pairs[2k] = src,
+ * pairs[2k+1] = dst (8-byte aligned; 16-byte aligned arrays take 128-bit loads
+ * of two pairs).  Async on stream. */
+int cbaa_update_pairs(cbaa_handle* h, const uint32_t* pairs, uint64_t n, cbaa_stream stream);
+
 /* Same as cbaa_update for HOST arrays (pinned or pageable): the library copies
  * them to the device in chunks on its own copy stream, double-buffered and
  * overlapped with the update kernels (the local-server buffer → GPU copy of

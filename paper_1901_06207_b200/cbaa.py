@@ -75,6 +75,7 @@ _SIGS = {
     "cbaa_reset": (C.c_int, [_h, C.c_void_p]),
     "cbaa_update": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "cbaa_update_host": (C.c_int, [_h, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "cbaa_update_pairs": (C.c_int, [_h, C.c_void_p, C.c_uint64, C.c_void_p]),
     "cbaa_skipped": (C.c_int, [_h, _P(C.c_uint64), C.c_void_p]),
     "cbaa_merge": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_uint64, C.c_void_p]),
     "cbaa_merge_slice": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_uint32, C.c_uint32, C.c_void_p]),
@@ -245,6 +246,11 @@ class Cbaa:
             raise ValueError("src and dst differ in length")
         self._check(lib().cbaa_update(self._h, _dptr(src, "src"), _dptr(dst, "dst"), src.numel(), _stream(stream)),
                     "cbaa_update")
+
+    def update_pairs(self, pairs, stream=None):
+        """Alg. 1 over one device tensor of interleaved (src, dst) pairs, shape (n, 2) or (2n,)."""
+        n = pairs.numel() // 2
+        self._check(lib().cbaa_update_pairs(self._h, _dptr(pairs, "pairs"), n, _stream(stream)), "cbaa_update_pairs")
 
     def update_host(self, src, dst, stream=None):
         """Alg. 1 over HOST arrays (numpy or CPU tensors, ideally pinned): pipelined H2D inside the library."""

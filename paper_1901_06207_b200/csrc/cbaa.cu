@@ -338,6 +338,43 @@ int launch_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   return launch_check(h, "k_update");
 }
 
+// One pass of Alg. 1 over n interleaved device pairs (src, dst, src, dst, ...).
+int launch_update_aos(cbaa_handle* h, const uint32_t* pairs, uint64_t n, uint32_t lo, uint32_t span,
+                      bool count_skips, cudaStream_t s) {
+  const uintptr_t a = (uintptr_t)pairs;
+  const uint64_t head = std::min<uint64_t>(n, (a & 15) ? 1 : 0);   // 8-B aligned: at most one pair to peel
+  const uint64_t n8 = (n - head) / 8;
+  const uint64_t scalar = head + (n - head - 8 * n8);
+  const int grid = grid_for(h, std::max(n8, scalar), h->upd_blocks);
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
+  unsigned long long* sk = count_skips ? h->skipped : nullptr;
+  const Geo& G = h->G;
+  const uint2* p2 = (const uint2*)pairs;
+  const bool paper = G.num_ra == 3 && G.num_va == 1;
+#define CBAA_LAUNCH_AOS(NRA, NVA, MODE, PFX) \
+  k_update_aos<NRA, NVA, MODE, PFX><<<grid, kThreads, 0, s>>>(G, p2, head, n8, n, h->cube, lo, span, sk)
+  if (paper) {
+    if (test) {
+      if (prefix) CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_TEST_SET, true);
+      else CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_TEST_SET, false);
+    } else {
+      if (prefix) CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_RED, true);
+      else CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_RED, false);
+    }
+  } else {
+    if (test) {
+      if (prefix) CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_TEST_SET, true);
+      else CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_TEST_SET, false);
+    } else {
+      if (prefix) CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_RED, true);
+      else CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_RED, false);
+    }
+  }
+#undef CBAA_LAUNCH_AOS
+  return launch_check(h, "k_update_aos");
+}
+
 int update_all_passes(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t W = h->cube_words;
   for (uint32_t p = 0; p < h->passes; ++p) {
@@ -515,6 +552,21 @@ int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64
   if (((uintptr_t)src | (uintptr_t)dst) & 3) return fail(h, CBAA_E_ARG, "cbaa_update: src/dst must be 4-byte aligned");
   DeviceGuard dg(h->device);
   return update_all_passes(h, src, dst, n, (cudaStream_t)stream);
+}
+
+int cbaa_update_pairs(cbaa_handle* h, const uint32_t* pairs, uint64_t n, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (n == 0) return CBAA_OK;
+  if (!pairs) return fail(h, CBAA_E_ARG, "cbaa_update_pairs: null pairs");
+  if ((uintptr_t)pairs & 7) return fail(h, CBAA_E_ARG, "cbaa_update_pairs: pairs must be 8-byte aligned");
+  DeviceGuard dg(h->device);
+  const uint64_t W = h->cube_words;
+  for (uint32_t p = 0; p < h->passes; ++p) {
+    uint64_t lo = W * p / h->passes, hi = W * (p + 1) / h->passes;
+    int rc = launch_update_aos(h, pairs, n, (uint32_t)lo, (uint32_t)(hi - lo), p == 0, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return CBAA_OK;
 }
 
 int cbaa_update_host(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream) {

@@ -208,6 +208,50 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo
   }
 }
 
+// Interleaved ("packed") pairs: pairs[2k] = src, pairs[2k+1] = dst, e.g. straight out of a capture
+// buffer.  One 16-B load carries two pairs; eight pairs per thread per step.  Pairs [0, head) and
+// [head + 8·n8, n) go one per thread; [head, head + 8·n8) is 16-B aligned.
+template <int NRA, int NVA, int MODE, bool PREFIX>
+__global__ void __launch_bounds__(kThreads) k_update_aos(const __grid_constant__ Geo G, const uint2* __restrict__ pairs,
+                                                         uint64_t head, uint64_t n8, uint64_t n,
+                                                         uint32_t* __restrict__ cube, uint32_t lo, uint32_t span,
+                                                         unsigned long long* __restrict__ skipped) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t skip = 0;
+  const uint64_t tail0 = head + 8 * n8;
+  for (int t = 0; t < 2; ++t) {
+    const uint64_t k = t == 0 ? gid : tail0 + gid;
+    if ((t == 0 && k < head) || (t == 1 && k < n)) {
+      uint2 pr = pairs[k];
+      uint32_t s = pr.x, d = pr.y;
+      if (normalize<PREFIX>(G, s, d)) set_pair_generic<MODE>(G, s, d, cube, lo, span);
+      else ++skip;
+    }
+  }
+  const uint4* p4 = reinterpret_cast<const uint4*>(pairs + head);
+  for (uint64_t i = gid; i < n8; i += stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcs(p4 + 4 * i + q);
+    uint32_t ss[8] = {v[0].x, v[0].z, v[1].x, v[1].z, v[2].x, v[2].z, v[3].x, v[3].z};
+    uint32_t dd[8] = {v[0].y, v[0].w, v[1].y, v[1].w, v[2].y, v[2].w, v[3].y, v[3].w};
+    if (NRA) {
+      set_quad<(NRA ? NRA : 1), NVA, MODE, PREFIX>(G, ss, dd, cube, lo, span, skip);
+      set_quad<(NRA ? NRA : 1), NVA, MODE, PREFIX>(G, ss + 4, dd + 4, cube, lo, span, skip);
+    } else {
+      for (int p = 0; p < 8; ++p) {
+        if (normalize<PREFIX>(G, ss[p], dd[p])) set_pair_generic<MODE>(G, ss[p], dd[p], cube, lo, span);
+        else ++skip;
+      }
+    }
+  }
+  if (PREFIX && skipped) {
+    skip = warp_sum(skip);
+    if ((threadIdx.x & 31) == 0 && skip) atomicAdd(skipped, (unsigned long long)skip);
+  }
+}
+
 // ---------------------------------------------------------------- reset / merge
 __global__ void __launch_bounds__(kThreads) k_zero(uint4* __restrict__ p, uint64_t n16) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

@@ -437,3 +437,21 @@ def test_zero_count_paths(paper, no_tma, monkeypatch):
     st, oh, ostats = O.detect(paper, ref, 1024)
     assert_stats_equal(stats, ostats)
     assert_hosts_equal(hosts, oh)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n, off", [(1_000_003, 0), (1_000_003, 1), (7, 0), (9, 1), (0, 0)])
+def test_update_interleaved_pairs(paper, n, off, mode):
+    """cbaa_update_pairs on interleaved (src, dst) arrays: 16-B aligned, 8-B aligned (one pair peeled),
+    ragged tails — same cube as the oracle."""
+    src, dst = W.random_pairs(max(n, 1), 40 + n)
+    src, dst = src[:n], dst[:n]
+    inter = np.zeros(2 * (n + 1), np.uint32)
+    inter[2 * off: 2 * off + 2 * n: 2] = src
+    inter[2 * off + 1: 2 * off + 2 * n: 2] = dst
+    t = dev(inter)[2 * off: 2 * off + 2 * n]
+    cb = handle(paper, update_mode=mode)
+    cb.reset()
+    cb.update_pairs(t)
+    ref, _ = O.update(paper, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
