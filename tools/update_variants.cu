@@ -116,24 +116,10 @@ __global__ void __launch_bounds__(kThreads) kx_update_keep(const __grid_constant
 constexpr int kTile = 2048;   // pairs per tile: 8 KB src + 8 KB dst per stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
-  }
-}
-
 __global__ void __launch_bounds__(kThreads) kx_update_tma(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
                                                           const uint32_t* __restrict__ dst, uint64_t n,
                                                           uint32_t* __restrict__ cube, uint32_t lo, uint32_t span) {
@@ -219,6 +205,23 @@ __global__ void __launch_bounds__(kThreads) kx_update_na(const __grid_constant__
   }
 }
 
+// V11/V12: the product's 8-pair body with a register budget for 3 / 4 CTAs per SM.
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) kx_update_lb(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
+                                                               const uint32_t* __restrict__ dst, uint64_t n8,
+                                                               uint32_t* __restrict__ cube, uint32_t lo, uint32_t span) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t skip = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+    uint4 sa = ld_stream4(src + 8 * i), sb = ld_stream4(src + 8 * i + 4);
+    uint4 da = ld_stream4(dst + 8 * i), db = ld_stream4(dst + 8 * i + 4);
+    uint32_t ss[4] = {sa.x, sa.y, sa.z, sa.w}, dd[4] = {da.x, da.y, da.z, da.w};
+    uint32_t ss2[4] = {sb.x, sb.y, sb.z, sb.w}, dd2[4] = {db.x, db.y, db.z, db.w};
+    set_quad<3, 1, CBAA_UPDATE_TEST_SET, false>(G, ss, dd, cube, lo, span, skip);
+    set_quad<3, 1, CBAA_UPDATE_TEST_SET, false>(G, ss2, dd2, cube, lo, span, skip);
+  }
+}
+
 }  // namespace cbaa
 
 extern "C" int cbaa_x_update(cbaa_handle* h, int variant, int passes, int blocks_per_sm, const uint32_t* src,
@@ -236,6 +239,8 @@ extern "C" int cbaa_x_update(cbaa_handle* h, int variant, int passes, int blocks
       case 4: kx_update_filter<13><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 4, h->cube, lo, hi - lo); break;
       case 5: kx_update_keep<<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 4, h->cube, lo, hi - lo); break;
       case 8: kx_update_tma<<<grid, kThreads, 0, s>>>(h->G, src, dst, n, h->cube, lo, hi - lo); break;
+      case 11: kx_update_lb<3><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 12: kx_update_lb<4><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 9: kx_update_na<false><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 10: kx_update_na<true><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 6:
