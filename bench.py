@@ -152,6 +152,17 @@ def ncu_traffic():
         return None
 
 
+def ncu_update_counters():
+    """Per-launch L1/L2 utilisation of k_update from the committed ncu --set full capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_counters.json")))
+        ls = [e for e in d["launches"] if "k_update" in e["kernel"]]
+        keys = ("lts_throughput_avg_pct", "lts_throughput_max_pct", "l1tex_throughput_pct", "l1_hit_pct", "l2_hit_pct")
+        return {k: [round(e[k], 1) for e in ls] for k in keys} | {"source": "profiles/r01_ncu_counters.json"}
+    except Exception:
+        return None
+
+
 # --------------------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank, world, _ = dist_env()
@@ -422,7 +433,7 @@ def main():
                 "peak_ldg": peaks_acc.get("ldg", 0) / 1e9, "peak_ldg_ca": peaks_acc.get("ldg_ca", 0) / 1e9,
                 "peak_red": peaks_acc.get("red", 0) / 1e9,
                 "update_ms": upd, "launch_ms": upd / passes, "update_passes": passes,
-                "update_mode": args.update_mode}
+                "update_mode": args.update_mode, "ncu_per_pass": ncu_update_counters()}
     roofline_hbm = {"bound": "hbm", "achieved": 8 * n / (upd / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": 8 * n / (upd / 1e3) / 1e9 / hbm,
                     "note": "input stream, 8 B/pair algorithmic; peak = MEASURED_PEAKS.json hbm_gbs"}
