@@ -327,13 +327,28 @@ def main():
     # Pipelined windows (N = 1): two cubes; window k's reset+update run on the update stream while
     # window k-1's detect runs on a high-priority stream (its 128-thread CTAs fit beside the persistent
     # update CTAs).  Cube k%2 is reset only after the detect of window k-2 has returned (host order).
-    pipelined = world == 1 and not args.no_pipeline
+    # Pipelined windows: two cubes; window k's reset+update run on the update stream while window k-1's
+    # [exchange +] detect runs on a high-priority stream (its kernels fit beside the persistent update
+    # CTAs).  Cube k%2 is reset only after the detect of window k-2 has returned on every rank (host
+    # order; at N > 1 the ipc exchange's window_done barrier).  N > 1 pipelines with the ipc exchange.
+    pipelined = not args.no_pipeline and (world == 1 or exchange == "ipc")
     if pipelined:
         cfg.detect_overlap = 1             # window-end kernels without shared memory: they co-run
         cbs = [Cbaa(cfg, local), Cbaa(cfg, local)]
         cb2 = cbs[1]
+        peers = [D.IpcExchange(c, rank, world) for c in cbs] if world > 1 else [None, None]
         lo_pri, hi_pri = torch.cuda.Stream.priority_range()
         s_upd, s_det = stream, torch.cuda.Stream(priority=hi_pri)
+
+        def finish(c, pe, px):
+            s_det.wait_event(pe)
+            lo, hi = 0, n_cs
+            if px:
+                lo, hi = px.exchange(c, rank, world, n_cs, cs_bytes, s_det)
+            out, _, _ = c.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s_det)
+            if px:
+                px.window_done(s_det)
+            return D.gather_hosts(out, rank, world)
 
         def run_pipelined(n_win, upd_evs=None):
             pending, out = None, None
@@ -348,29 +363,33 @@ def main():
                 if upd_evs:
                     upd_evs[k][1].record(s_upd)
                 if pending:
-                    pc, pe = pending
-                    s_det.wait_event(pe)
-                    out, _, _ = pc.detect(THETA, stream=s_det)
-                pending = (c, done)
-            pc, pe = pending
-            s_det.wait_event(pe)
-            out, _, _ = pc.detect(THETA, stream=s_det)
-            return out
+                    out = finish(*pending)
+                pending = (c, done, peers[k % 2])
+            return finish(*pending)
 
         run_pipelined(max(args.warmup, 3))
         torch.cuda.synchronize()
         launches0 = cbs[0].kernel_launches + cb2.kernel_launches
         pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
         p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
             p_start.record(s_upd)
             hosts = run_pipelined(args.steps, pevs)
             p_end.record(s_det)
             torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         launches = cbs[0].kernel_launches + cb2.kernel_launches - launches0
         elapsed_ms = p_start.elapsed_time(p_end)
+        if world > 1:
+            elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
         upd_ms = [e[0].elapsed_time(e[1]) for e in pevs]
+        for px in peers:
+            if px:
+                px.close()
 
     # window-end detect latency alone: update finished, then detect until the host list is filled
     det_ms = []
@@ -443,7 +462,8 @@ def main():
             "config": dict(config_block(args.workload, spec, world), exchange=exchange),
             "detect_ms": statistics.median(det_ms), "update_ms": upd,
             "post_update_ms": statistics.median(post_ms),
-            "windows": "pipelined: detect(k) overlaps reset+update(k+1), two cubes" if pipelined else "serial",
+            "windows": ("pipelined: [exchange +] detect(k) overlaps reset+update(k+1), two cubes" if pipelined
+                        else "serial"),
             "ms_per_step_serial": serial_ms / args.steps,
             "update_pairs_per_s": n * world / (upd / 1e3),
             "n_super_hosts": int(len(hosts)) if hosts is not None else None,
