@@ -340,7 +340,14 @@ def main():
         lo_pri, hi_pri = torch.cuda.Stream.priority_range()
         s_upd, s_det = stream, torch.cuda.Stream(priority=hi_pri)
 
-        def finish(c, pe, px):
+        # the window reset moves to the detect stream: cube k%2 is cleared right after its detect (and,
+        # at N > 1, after every peer has finished reading it), overlapping the other cube's update
+        clean = [torch.cuda.Event(), torch.cuda.Event()]
+        for i, c in enumerate(cbs):
+            c.reset(s_det)
+            clean[i].record(s_det)
+
+        def finish(c, pe, px, i):
             s_det.wait_event(pe)
             lo, hi = 0, n_cs
             if px:
@@ -348,13 +355,15 @@ def main():
             out, _, _ = c.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s_det)
             if px:
                 px.window_done(s_det)
+            c.reset(s_det)
+            clean[i].record(s_det)
             return D.gather_hosts(out, rank, world)
 
         def run_pipelined(n_win, upd_evs=None):
             pending, out = None, None
             for k in range(n_win):
                 c = cbs[k % 2]
-                c.reset(s_upd)
+                s_upd.wait_event(clean[k % 2])
                 if upd_evs:
                     upd_evs[k][0].record(s_upd)
                 c.update(src, dst, s_upd)
@@ -364,7 +373,7 @@ def main():
                     upd_evs[k][1].record(s_upd)
                 if pending:
                     out = finish(*pending)
-                pending = (c, done, peers[k % 2])
+                pending = (c, done, peers[k % 2], k % 2)
             return finish(*pending)
 
         run_pipelined(max(args.warmup, 3))
@@ -462,7 +471,7 @@ def main():
             "config": dict(config_block(args.workload, spec, world), exchange=exchange),
             "detect_ms": statistics.median(det_ms), "update_ms": upd,
             "post_update_ms": statistics.median(post_ms),
-            "windows": ("pipelined: [exchange +] detect(k) overlaps reset+update(k+1), two cubes" if pipelined
+            "windows": ("pipelined: [exchange +] detect(k) + reset overlap update(k+1), two cubes" if pipelined
                         else "serial"),
             "ms_per_step_serial": serial_ms / args.steps,
             "update_pairs_per_s": n * world / (upd / 1e3),
