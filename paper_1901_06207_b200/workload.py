@@ -56,7 +56,7 @@ def c4_spec(n_shard=250_000_000, scale=1.0, seed=4):
     sc = tuple(int(x) for x in rng.integers(2000, 20001, 50))
     vi = tuple(int(x) for x in rng.integers(5000, 30001, 20))
     return WindowSpec(n=int(n_shard * scale), n_hosts=int(1_200_000 * scale), n_flows=int(16_000_000 * scale),
-                      scanners=sc, victims=vi, victim_share=0.05)
+                      scanners=sc, victims=vi, victim_share=0.05, n_prefixes=32)
 
 
 def c5_geometries():
