@@ -179,7 +179,17 @@ __device__ __forceinline__ uint32_t ld_cube_keep(const uint32_t* p) {
   asm volatile("ld.global.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-template <bool KEEP>
+__device__ __forceinline__ uint32_t ld_cube_first(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_cube_unchanged(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.L1::evict_unchanged.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+template <int KEEP>
 __global__ void __launch_bounds__(kThreads) kx_update_na(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
                                                          const uint32_t* __restrict__ dst, uint64_t n8,
                                                          uint32_t* __restrict__ cube, uint32_t lo, uint32_t span) {
@@ -196,7 +206,10 @@ __global__ void __launch_bounds__(kThreads) kx_update_na(const __grid_constant__
     for (int p = 0; p < 8; ++p)
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-        v[p][a] = w[p][a] == kNoWord ? bit[p] : (KEEP ? ld_cube_keep(cube + w[p][a]) : __ldca(cube + w[p][a]));
+        v[p][a] = w[p][a] == kNoWord ? bit[p]
+                  : (KEEP == 1 ? ld_cube_keep(cube + w[p][a])
+                     : KEEP == 2 ? ld_cube_first(cube + w[p][a])
+                     : KEEP == 3 ? ld_cube_unchanged(cube + w[p][a]) : __ldca(cube + w[p][a]));
 #pragma unroll
     for (int p = 0; p < 8; ++p)
 #pragma unroll
@@ -241,8 +254,10 @@ extern "C" int cbaa_x_update(cbaa_handle* h, int variant, int passes, int blocks
       case 8: kx_update_tma<<<grid, kThreads, 0, s>>>(h->G, src, dst, n, h->cube, lo, hi - lo); break;
       case 11: kx_update_lb<3><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 12: kx_update_lb<4><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
-      case 9: kx_update_na<false><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
-      case 10: kx_update_na<true><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 9: kx_update_na<0><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 10: kx_update_na<1><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 13: kx_update_na<2><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 14: kx_update_na<3><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 6:
       case 7: {  // product kernel with the smem carveout forced to 0 (max L1) / to max smem (min L1)
         cudaFuncSetAttribute(k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
