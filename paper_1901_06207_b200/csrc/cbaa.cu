@@ -11,6 +11,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "cbaa.h"
@@ -298,6 +299,28 @@ int grid_for(const cbaa_handle* h, uint64_t work_items, int per_sm) {
   return (int)std::max<uint64_t>(1, std::min(want, cap));
 }
 
+// Calls f(NRA, NVA, MODE, PREFIX) with the compile-time variant of the update kernels that matches the
+// handle: the paper shape (|RA| = 3, |VA| = 1) or the generic geometry, test-and-set or plain RED, and
+// normalised or inner-prefix input.
+template <class F>
+void dispatch_update(const cbaa_handle* h, F&& f) {
+  using T = std::integral_constant<int, CBAA_UPDATE_TEST_SET>;
+  using R = std::integral_constant<int, CBAA_UPDATE_RED>;
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
+  auto go = [&](auto nra, auto nva) {
+    if (test) {
+      if (prefix) f(nra, nva, T{}, std::true_type{});
+      else f(nra, nva, T{}, std::false_type{});
+    } else {
+      if (prefix) f(nra, nva, R{}, std::true_type{});
+      else f(nra, nva, R{}, std::false_type{});
+    }
+  };
+  if (h->G.num_ra == 3 && h->G.num_va == 1) go(std::integral_constant<int, 3>{}, std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
+}
+
 // One pass of Alg. 1 over n device pairs, restricted to cube words [lo, lo+span).
 int launch_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t lo, uint32_t span,
                   bool count_skips, cudaStream_t s) {
@@ -308,33 +331,12 @@ int launch_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   uint64_t n4 = vec ? (n - head) / 4 : 0;
   if (!vec) head = n;   // everything scalar
   uint64_t scalar = head + (n - head - 4 * n4);
-  uint64_t items = std::max(n4, scalar);
-  int grid = grid_for(h, items, h->upd_blocks);
-  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
+  const int grid = grid_for(h, std::max(n4, scalar), h->upd_blocks);
   unsigned long long* sk = count_skips ? h->skipped : nullptr;
-  const Geo& G = h->G;
-  const bool paper = G.num_ra == 3 && G.num_va == 1;
-#define CBAA_LAUNCH_UPD(NRA, NVA, MODE, PFX) \
-  k_update<NRA, NVA, MODE, PFX><<<grid, kThreads, 0, s>>>(G, src, dst, head, n4, n, h->cube, lo, span, sk)
-  if (paper) {
-    if (test) {
-      if (prefix) CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_TEST_SET, true);
-      else CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_TEST_SET, false);
-    } else {
-      if (prefix) CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_RED, true);
-      else CBAA_LAUNCH_UPD(3, 1, CBAA_UPDATE_RED, false);
-    }
-  } else {
-    if (test) {
-      if (prefix) CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_TEST_SET, true);
-      else CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_TEST_SET, false);
-    } else {
-      if (prefix) CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_RED, true);
-      else CBAA_LAUNCH_UPD(0, 0, CBAA_UPDATE_RED, false);
-    }
-  }
-#undef CBAA_LAUNCH_UPD
+  dispatch_update(h, [&](auto nra, auto nva, auto mode, auto pfx) {
+    k_update<decltype(nra)::value, decltype(nva)::value, decltype(mode)::value, decltype(pfx)::value>
+        <<<grid, kThreads, 0, s>>>(h->G, src, dst, head, n4, n, h->cube, lo, span, sk);
+  });
   return launch_check(h, "k_update");
 }
 
@@ -346,32 +348,12 @@ int launch_update_aos(cbaa_handle* h, const uint32_t* pairs, uint64_t n, uint32_
   const uint64_t n8 = (n - head) / 8;
   const uint64_t scalar = head + (n - head - 8 * n8);
   const int grid = grid_for(h, std::max(n8, scalar), h->upd_blocks);
-  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
   unsigned long long* sk = count_skips ? h->skipped : nullptr;
-  const Geo& G = h->G;
   const uint2* p2 = (const uint2*)pairs;
-  const bool paper = G.num_ra == 3 && G.num_va == 1;
-#define CBAA_LAUNCH_AOS(NRA, NVA, MODE, PFX) \
-  k_update_aos<NRA, NVA, MODE, PFX><<<grid, kThreads, 0, s>>>(G, p2, head, n8, n, h->cube, lo, span, sk)
-  if (paper) {
-    if (test) {
-      if (prefix) CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_TEST_SET, true);
-      else CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_TEST_SET, false);
-    } else {
-      if (prefix) CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_RED, true);
-      else CBAA_LAUNCH_AOS(3, 1, CBAA_UPDATE_RED, false);
-    }
-  } else {
-    if (test) {
-      if (prefix) CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_TEST_SET, true);
-      else CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_TEST_SET, false);
-    } else {
-      if (prefix) CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_RED, true);
-      else CBAA_LAUNCH_AOS(0, 0, CBAA_UPDATE_RED, false);
-    }
-  }
-#undef CBAA_LAUNCH_AOS
+  dispatch_update(h, [&](auto nra, auto nva, auto mode, auto pfx) {
+    k_update_aos<decltype(nra)::value, decltype(nva)::value, decltype(mode)::value, decltype(pfx)::value>
+        <<<grid, kThreads, 0, s>>>(h->G, p2, head, n8, n, h->cube, lo, span, sk);
+  });
   return launch_check(h, "k_update_aos");
 }
 
