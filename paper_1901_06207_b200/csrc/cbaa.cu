@@ -222,7 +222,7 @@ int alloc_scratch(cbaa_handle* h) {
   const size_t n_cs = G.n_cs;
   const uint32_t hit_cap = h->cfg.hit_capacity ? h->cfg.hit_capacity : (1u << 20);
   // header: ztot[n_cs] done[n_cs] done_all n_cand skipped — zeroed per detect (skipped per reset);
-  // n_hits is zeroed by k_zero_hot
+  // n_hits is zeroed by the zero-count kernel
   size_t off = 0;
   size_t o_ztot = off;
   off += n_cs * 8;
@@ -688,9 +688,9 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t n_range = cs_hi - cs_lo;
   DetectScratch& D = h->D;
-  // The whole device side of a detect — zeroing, k_zero_hot, k_tuples and the copy of the CS records
-  // and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured once per
-  // (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
+  // The whole device side of a detect — zeroing, zero counts, k_hot, the Alg. 3 kernels and the copy
+  // of the CS records and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured
+  // once per (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
   const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
   const DetectKey key{cs_lo, cs_hi, theta, h->record, (const void*)D.cand, (const void*)h->h_res, h->use_join};
   if (!h->graph_exec || !(h->graph_key == key)) {
