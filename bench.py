@@ -288,7 +288,7 @@ def main():
                     lo, hi = peer.exchange(cb, rank, world, n_cs, cs_bytes, stream)
                 else:
                     lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
-        hosts, stats, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream)
+        hosts, _, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream, with_stats=False)
         if exchange == "p2p":
             with torch.cuda.stream(stream):
                 peer.window_done()
@@ -352,7 +352,7 @@ def main():
             lo, hi = 0, n_cs
             if px:
                 lo, hi = px.exchange(c, rank, world, n_cs, cs_bytes, s_det)
-            out, _, _ = c.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s_det)
+            out, _, _ = c.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s_det, with_stats=False)
             if px:
                 px.window_done(s_det)
             c.reset(s_det)
@@ -406,7 +406,7 @@ def main():
         for _ in range(10):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            h, _, _ = cb.detect(THETA, stream=stream)
+            h, _, _ = cb.detect(THETA, stream=stream, with_stats=False)
             det_ms.append(1e3 * (time.perf_counter() - t0))
 
     e2e = None

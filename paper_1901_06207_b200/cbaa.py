@@ -290,19 +290,21 @@ class Cbaa:
                     "cbaa_merge_slice")
 
     def detect(self, theta: int, cap: int = 1 << 20, cs_lo: int = 0, cs_hi: int | None = None, stream=None,
-               raise_on_overflow: bool = False):
-        """Window end: returns (hosts structured array, per-CS stats list, status code)."""
+               raise_on_overflow: bool = False, with_stats: bool = True):
+        """Window end: returns (hosts structured array, per-CS stats list or None, status code)."""
         cs_hi = self.n_cs if cs_hi is None else cs_hi
         out = getattr(self, "_out", None)
         if out is None or out.size < max(cap, 1):
             out = self._out = np.empty(max(cap, 1), dtype=HOST_DTYPE)   # reused across windows
-        stats = (CsStats * (cs_hi - cs_lo))()
+        stats = (CsStats * (cs_hi - cs_lo))() if with_stats else None
         n = C.c_uint64()
         rc = lib().cbaa_detect_range(self._h, theta, cs_lo, cs_hi, out.ctypes.data_as(C.c_void_p), cap,
                                      C.byref(n), stats, _stream(stream))
         allow = () if raise_on_overflow else (E_TUPLE_CAP,)
         self._check(rc, "cbaa_detect", allow=allow)
         hosts = out[: min(n.value, cap)].copy()
+        if stats is None:
+            return hosts, None, rc
         sd = [dict(ztot=s.ztot, eta=s.eta, eps=s.eps, theta_bn=s.theta_bn, zmax=s.zmax,
                    n_hot=list(s.n_hot[: self.cfg.num_ra]), tuples=s.tuples, candidates=s.candidates, hits=s.hits,
                    overflow=s.overflow) for s in stats]

@@ -723,6 +723,12 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
         rc = launch_check(h, "k_tuples");
       }
     }
+    // S:418 order on the device (a standalone detect; with detect_overlap the host sorts, because the
+    // sort's shared memory would keep it from running beside another handle's update)
+    if (!rc && !h->cfg.detect_overlap) {
+      k_sort_hits<<<1, 1024, 0, c>>>(D);
+      rc = launch_check(h, "k_sort_hits");
+    }
     cudaMemcpyAsync(h->h_rec, D.rec + cs_lo, (size_t)n_range * sizeof(cbaa_cs_stats), cudaMemcpyDeviceToHost, c);
     cudaMemcpyAsync(h->h_res, D.n_hits, 64 + kFirst * sizeof(cbaa_host), cudaMemcpyDeviceToHost, c);
     cudaGraph_t graph = nullptr;
@@ -736,7 +742,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
     h->graph_key = key;
-    h->graph_kernels = join ? 4 : 3;
+    h->graph_kernels = (join ? 4 : 3) + (h->cfg.detect_overlap ? 0 : 1);
     h->launches -= h->graph_kernels;   // counted at capture; counted again per graph launch below
   }
   CK(h, cudaGraphLaunch(h->graph_exec, s));
@@ -767,11 +773,13 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
                           cudaMemcpyDeviceToHost, s));
     CK(h, cudaStreamSynchronize(s));
   }
-  // output order of S:418: estimate descending, then ip ascending
-  std::sort(h->h_hits, h->h_hits + got, [](const cbaa_host& a, const cbaa_host& b) {
-    if (a.estimate != b.estimate) return a.estimate > b.estimate;
-    return a.ip < b.ip;
-  });
+  // output order of S:418: estimate descending, then ip ascending (already done on the device for a
+  // standalone detect of at most kSortMax hits)
+  if (h->cfg.detect_overlap || got > (uint64_t)kSortMax)
+    std::sort(h->h_hits, h->h_hits + got, [](const cbaa_host& a, const cbaa_host& b) {
+      if (a.estimate != b.estimate) return a.estimate > b.estimate;
+      return a.ip < b.ip;
+    });
   const uint64_t ncopy = std::min<uint64_t>(got, cap);
   if (ncopy) std::memcpy(out, h->h_hits, ncopy * sizeof(cbaa_host));
   *n_out = total;

@@ -817,6 +817,57 @@ __global__ void __launch_bounds__(kDetThreads) k_union(const __grid_constant__ G
   }
 }
 
+// Output order of S:418 (estimate descending, then ip ascending) on the device: one CTA bitonic-sorts up to
+// kSortMax hits in shared memory, so the host copies them out already ordered.  More hits: left to the
+// host (the library sorts there).
+constexpr int kSortMax = 2048;
+__global__ void __launch_bounds__(1024) k_sort_hits(const __grid_constant__ DetectScratch D) {
+  __shared__ unsigned long long s_est[kSortMax];
+  __shared__ uint32_t s_ip[kSortMax];
+  __shared__ uint16_t s_idx[kSortMax];
+  const unsigned long long n = min(*D.n_hits, (unsigned long long)D.hit_cap);
+  if (n <= 1 || n > (unsigned long long)kSortMax) return;
+  uint32_t m = 1;
+  while (m < n) m <<= 1;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const bool v = i < n;
+    // estimates are ≥ 0 (or +inf): their IEEE bits order like the values
+    s_est[i] = v ? (unsigned long long)__double_as_longlong(D.hits[i].estimate) : 0ull;
+    s_ip[i] = v ? D.hits[i].ip : 0xffffffffu;
+    s_idx[i] = (uint16_t)i;
+  }
+  __syncthreads();
+  // "before(a, b)": a comes first in the output; padding (index ≥ n) always last
+  auto before = [&](uint32_t a, uint32_t b) {
+    const bool va = s_idx[a] < n, vb = s_idx[b] < n;
+    if (va != vb) return va;
+    return s_est[a] != s_est[b] ? s_est[a] > s_est[b] : s_ip[a] < s_ip[b];
+  };
+  for (uint32_t k = 2; k <= m; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          if (up ? before(l, i) : before(i, l)) {
+            unsigned long long te = s_est[i]; s_est[i] = s_est[l]; s_est[l] = te;
+            uint32_t ti = s_ip[i]; s_ip[i] = s_ip[l]; s_ip[l] = ti;
+            uint16_t tx = s_idx[i]; s_idx[i] = s_idx[l]; s_idx[l] = tx;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // gather through registers: read every hit first, then write the permuted order
+  cbaa_host tmp[2];
+  uint32_t cnt = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) tmp[cnt++] = D.hits[s_idx[i]];
+  __syncthreads();
+  cnt = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) D.hits[i] = tmp[cnt++];
+}
+
 // Alg. 1 mapping for the unit parity tests (no cube access).
 __global__ void k_debug_map(const __grid_constant__ Geo G, const uint32_t* __restrict__ iip,
                             const uint32_t* __restrict__ oip, uint64_t n, uint32_t* __restrict__ cs_out,
