@@ -317,7 +317,14 @@ void dispatch_update(const cbaa_handle* h, F&& f) {
       else f(nra, nva, R{}, std::false_type{});
     }
   };
+  using RT = std::integral_constant<int, -1>;   // RA/VA split at run time
+  const uint32_t na = h->G.narr;
   if (h->G.num_ra == 3 && h->G.num_va == 1) go(std::integral_constant<int, 3>{}, std::integral_constant<int, 1>{});
+  else if (na == 2) go(std::integral_constant<int, 2>{}, RT{});
+  else if (na == 3) go(std::integral_constant<int, 3>{}, RT{});
+  else if (na == 4) go(std::integral_constant<int, 4>{}, RT{});
+  else if (na == 5) go(std::integral_constant<int, 5>{}, RT{});
+  else if (na == 6) go(std::integral_constant<int, 6>{}, RT{});
   else go(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
 }
 

@@ -90,6 +90,29 @@ __device__ __forceinline__ uint32_t pair_targets(const Geo& G, uint32_t iip, uin
   return 1u << (row & 31);
 }
 
+// Any shape with NA = |RA| + |VA| arrays known at compile time and the RA/VA split at run time
+// (NVA < 0 in the templates below): the same word indices as pair_targets, array by array.
+template <int NA>
+__device__ __forceinline__ uint32_t pair_targets_rt(const Geo& G, uint32_t iip, uint32_t oip, uint32_t lo, uint32_t span,
+                                                    uint32_t* w) {
+  uint32_t mi = G.mangle_a * iip + G.mangle_b;
+  uint32_t mo = G.mangle_a * oip + G.mangle_b;
+  uint32_t cs = mi & G.rmask;
+  uint32_t lp = mi >> G.r;
+  uint32_t row = mix32(mo ^ G.bv_seed) & (G.g - 1);
+  uint32_t base = cs * G.cs_words + (row >> 5);
+  uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    const bool ra = a < (int)G.num_ra;
+    uint32_t col = ra ? (uint32_t)(dbl >> G.sh[a < CBAA_MAX_RA ? a : 0]) & G.colmask[a]   // CL(i)
+                      : mix32(lp ^ G.va_seeds[(a - G.num_ra) & (CBAA_MAX_VA - 1)]) & G.colmask[a];   // H_j
+    uint32_t x = base + G.arr_off[a] + (col << G.wpc_log2);
+    w[a] = x - lo < span ? x : kNoWord;
+  }
+  return 1u << (row & 31);
+}
+
 // Generic geometry (runtime |RA|, |VA|): one pair at a time.
 template <int MODE>
 __device__ __forceinline__ void set_pair_generic(const Geo& G, uint32_t iip, uint32_t oip, uint32_t* __restrict__ cube,
@@ -119,13 +142,14 @@ __device__ __forceinline__ void set_pair_generic(const Geo& G, uint32_t iip, uin
 template <int NRA, int NVA, int MODE, bool PREFIX>
 __device__ __forceinline__ void set_quad(const Geo& G, uint32_t* ss, uint32_t* dd, uint32_t* __restrict__ cube,
                                          uint32_t lo, uint32_t span, uint32_t& skip) {
-  constexpr int NA = NRA + NVA;
+  constexpr int NA = NVA < 0 ? NRA : NRA + NVA;
   uint32_t w[4][NA], bit[4];
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     bool ok = normalize<PREFIX>(G, ss[p], dd[p]);
     skip += ok ? 0u : 1u;
-    bit[p] = pair_targets<NRA, NVA>(G, ss[p], dd[p], lo, ok ? span : 0u, w[p]);
+    if constexpr (NVA < 0) bit[p] = pair_targets_rt<NA>(G, ss[p], dd[p], lo, ok ? span : 0u, w[p]);
+    else bit[p] = pair_targets<NRA, NVA>(G, ss[p], dd[p], lo, ok ? span : 0u, w[p]);
   }
   if (MODE == CBAA_UPDATE_TEST_SET) {
     uint32_t v[4][NA];
@@ -149,7 +173,8 @@ __device__ __forceinline__ void set_quad(const Geo& G, uint32_t* ss, uint32_t* d
 
 // Persistent grid-stride update.  Pairs [0, head) and [head + 4·n4, n) go one per thread;
 // [head, head + 4·n4) is 16-B aligned in both arrays and goes four per thread per step.
-// NRA = 0 selects the generic (runtime-geometry) path.
+// <3, 1>: the paper shape; <NA, -1>: NA arrays, RA/VA split at run time; <0, 0>: any geometry, one
+// pair at a time.
 template <int NRA, int NVA, int MODE, bool PREFIX>
 __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo G, const uint32_t* __restrict__ src,
                                                      const uint32_t* __restrict__ dst, uint64_t head, uint64_t n4,
