@@ -184,6 +184,8 @@ __device__ __forceinline__ uint32_t ld_cube_first(const uint32_t* p) {
   asm volatile("ld.global.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_cube_nc(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_cube_cg(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ uint32_t ld_cube_unchanged(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.L1::evict_unchanged.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -209,7 +211,9 @@ __global__ void __launch_bounds__(kThreads) kx_update_na(const __grid_constant__
         v[p][a] = w[p][a] == kNoWord ? bit[p]
                   : (KEEP == 1 ? ld_cube_keep(cube + w[p][a])
                      : KEEP == 2 ? ld_cube_first(cube + w[p][a])
-                     : KEEP == 3 ? ld_cube_unchanged(cube + w[p][a]) : __ldca(cube + w[p][a]));
+                     : KEEP == 3 ? ld_cube_unchanged(cube + w[p][a])
+                     : KEEP == 4 ? ld_cube_nc(cube + w[p][a])
+                     : KEEP == 5 ? ld_cube_cg(cube + w[p][a]) : __ldca(cube + w[p][a]));
 #pragma unroll
     for (int p = 0; p < 8; ++p)
 #pragma unroll
@@ -258,6 +262,8 @@ extern "C" int cbaa_x_update(cbaa_handle* h, int variant, int passes, int blocks
       case 10: kx_update_na<1><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 13: kx_update_na<2><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 14: kx_update_na<3><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 15: kx_update_na<4><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
+      case 16: kx_update_na<5><<<grid, kThreads, 0, s>>>(h->G, src, dst, n / 8, h->cube, lo, hi - lo); break;
       case 6:
       case 7: {  // product kernel with the smem carveout forced to 0 (max L1) / to max smem (min L1)
         cudaFuncSetAttribute(k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, cudaFuncAttributePreferredSharedMemoryCarveout,

@@ -48,7 +48,7 @@ def main():
     s = torch.cuda.current_stream()
     ref = None
     results = []
-    configs = [(0, 2, 2), (9, 2, 2), (13, 2, 2), (14, 2, 2), (13, 1, 2), (0, 2, 2)]
+    configs = [(0, 2, 2), (9, 2, 2), (15, 2, 2), (16, 2, 2), (15, 1, 2), (0, 2, 2)]
     for variant, passes, bps in configs:
         def run():
             h.reset()
