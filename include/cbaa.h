@@ -157,8 +157,12 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
 
 /* Alg. 1 for n pairs: src[k], dst[k] are DEVICE arrays of
  * host-order IPv4 (src = inner, dst = outer unless direction = INNER_PREFIX).
- * Sets |RA|+|VA| bits per pair with 32-bit atomic OR (Q11).  Any alignment is
- * accepted (16-B aligned arrays take the vector path).  Async on stream. */
+ * Sets |RA|+|VA| bits per pair with 32-bit atomic OR (Q11); with the default
+ * update_mode the word is loaded first and only a missing bit is ORed in — the
+ * cube is identical either way.  Updates accumulate until cbaa_reset; calls on
+ * one handle must be stream-ordered with its detect/merge/reset.  Any 4-byte
+ * alignment is accepted (16-B aligned arrays take the vector path).  Async on
+ * stream. */
 int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream);
 
 /* Same for interleaved ("packed") pairs in one DEVICE array: pairs[2k] = src,
