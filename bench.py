@@ -197,7 +197,7 @@ def cpu_baseline(w, seconds_budget=20.0):
     """The oracle as it stands, single-threaded, on a bounded sample of the same window."""
     from oracle import oracle as O
     p = O.default_params()
-    m = 10_000_000 if w.src.size >= 10_000_000 else w.src.size
+    m = min(w.src.size, 60_000_000)   # ~10-15 s of single-thread oracle work on the box's CPU
     t0 = time.perf_counter()
     cube, _ = O.update(p, w.src[:m], w.dst[:m])
     O.detect(p, cube, THETA)
