@@ -47,7 +47,6 @@ struct cbaa_handle {
   void* scratch = nullptr;
   DetectScratch D{};
   unsigned long long* skipped = nullptr;
-  size_t hdr_bytes = 0;   // bytes of the per-detect zeroed header (ztot, done, done_all, n_cand)
   // pinned host staging
   cbaa_cs_stats* h_rec = nullptr;
   unsigned long long* h_cnt = nullptr;
@@ -221,11 +220,8 @@ int alloc_scratch(cbaa_handle* h) {
   const Geo& G = h->G;
   const size_t n_cs = G.n_cs;
   const uint32_t hit_cap = h->cfg.hit_capacity ? h->cfg.hit_capacity : (1u << 20);
-  // header: ztot[n_cs] done[n_cs] done_all n_cand skipped — zeroed per detect (skipped per reset);
-  // n_hits is zeroed by the zero-count kernel
+  // counters: done[n_cs] done_all n_cand n_join (zeroed inside each detect), skipped (zeroed by reset)
   size_t off = 0;
-  size_t o_ztot = off;
-  off += n_cs * 8;
   size_t o_done = off;
   off += align_up(n_cs * 4, 8);
   size_t o_done_all = off;
@@ -234,7 +230,6 @@ int alloc_scratch(cbaa_handle* h) {
   off += 8;
   size_t o_njoin = off;
   off += 8;
-  h->hdr_bytes = off;
   size_t o_skipped = off;
   off += 8;
   off = align_up(off, 256);
@@ -260,7 +255,6 @@ int alloc_scratch(cbaa_handle* h) {
   CK(h, cudaMemset(base, 0, off));
   h->scratch = base;
   DetectScratch& D = h->D;
-  D.ztot = (unsigned long long*)(base + o_ztot);
   D.done = (unsigned int*)(base + o_done);
   D.done_all = (unsigned int*)(base + o_done_all);
   D.n_hits = (unsigned long long*)(base + o_nhits);
@@ -708,9 +702,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     if (!h->cap_stream) CK(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     cudaStream_t c = h->cap_stream;
     CK(h, cudaStreamBeginCapture(c, cudaStreamCaptureModeThreadLocal));
-    // per-detect zeroing: counters + the CS records of the range (candidates/hits accumulate)
-    cudaMemsetAsync(D.ztot, 0, h->hdr_bytes, c);
-    cudaMemsetAsync(D.rec + cs_lo, 0, (size_t)n_range * sizeof(cbaa_cs_stats), c);
+    // (the per-detect counters are zeroed inside the zero-count kernel and k_hot: no memset nodes)
     // |RA| = 3: range join over the sorted hot lists, then one warp per chain; otherwise (or after a
     // join-buffer overflow) the Cartesian enumeration with the union check inline
     const int join = h->use_join;

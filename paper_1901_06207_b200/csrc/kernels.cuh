@@ -332,7 +332,6 @@ struct DetectScratch {
   uint32_t* zc;                 // [n_cs][ra_cols]
   uint32_t* hc;                 // [n_cs][ra_cols], first n_hot[i] of each RA(i) block valid
   cbaa_cs_stats* rec;           // [n_cs]
-  unsigned long long* ztot;     // [n_cs] accumulators
   unsigned int* done;           // [n_cs] CTA arrival counters
   unsigned int* done_all;       // [1]
   unsigned long long* prefix;   // [n_range + 1] prefix of the work units of k_tuples (0 for overflowed CSs)
@@ -369,6 +368,19 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   __syncthreads();
   *total = tot;
   return before + incl - v;
+}
+
+// Per-detect counters, zeroed by CTA 0 of the zero-count kernel (everything that uses them runs in later
+// graph nodes): the k_hot arrival counters, the chain/candidate counters and the result-block head.
+__device__ __forceinline__ void zero_detect_counters(const DetectScratch& D, uint32_t cs_lo, uint32_t n_range) {
+  for (uint32_t k = threadIdx.x; k < n_range; k += blockDim.x) D.done[cs_lo + k] = 0;
+  if (threadIdx.x == 0) {
+    *D.done_all = 0;
+    *D.n_cand = 0;
+    *D.n_join = 0;
+    D.n_hits[0] = 0;
+    D.n_hits[1] = 0;   // result-block slot for the chain count (written by k_union)
+  }
 }
 
 // ---------------------------------------------------------------- TMA bulk-copy helpers
@@ -408,10 +420,7 @@ __global__ void __launch_bounds__(kDetThreads) k_zero_counts_tma(const __grid_co
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t tiles_per_cs = G.ra_cols / kZcTileCols;
   const uint64_t n_tiles = (uint64_t)n_range * tiles_per_cs;
-  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {
-    D.n_hits[0] = 0;
-    D.n_hits[1] = 0;
-  }
+  if (finish && blockIdx.x == 0) zero_detect_counters(D, cs_lo, n_range);
   if (threadIdx.x == 0) {
     for (int k = 0; k < kZcStages; ++k) mbar_init(&bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -433,20 +442,15 @@ __global__ void __launch_bounds__(kDetThreads) k_zero_counts_tma(const __grid_co
     mbar_wait(&bar[st], (it / kZcStages) & 1);
     const uint32_t cs = cs_lo + (uint32_t)(t / tiles_per_cs);
     const uint32_t col0 = (uint32_t)(t % tiles_per_cs) * kZcTileCols;
-    uint32_t zsum = 0;
 #pragma unroll
     for (int k = 0; k < (int)kZcTileCols / kDetWarps; ++k) {
       const uint32_t c = warp * (kZcTileCols / kDetWarps) + k;
       const uint4 v = tile[st][c * 32 + lane];
       const uint32_t pop = warp_sum(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w));
-      const uint32_t z = G.g - pop;                                      // zero bits
-      if (lane == 0) D.zc[(size_t)cs * G.ra_cols + col0 + c] = z;
-      zsum += z;
+      if (lane == 0) D.zc[(size_t)cs * G.ra_cols + col0 + c] = G.g - pop;   // zero bits
     }
     __syncthreads();   // the whole tile has been read: refill this stage
     if (threadIdx.x == 0 && t + (uint64_t)kZcStages * gridDim.x < n_tiles) issue(t + (uint64_t)kZcStages * gridDim.x, st);
-    // RA(0) columns are the first c(0) of the block: Ztot (Q12)
-    if (finish && lane == 0 && col0 < G.ncols[0]) atomicAdd(D.ztot + cs, (unsigned long long)zsum);
   }
 }
 
@@ -463,10 +467,7 @@ __global__ void __launch_bounds__(kDetThreads) k_zero_counts(const __grid_consta
   uint32_t gpc = 0;   // column groups per CS
   for (uint32_t i = 0; i < G.num_ra; ++i) gpc += (G.ncols[i] + kGroup - 1) / kGroup;
   const uint64_t total = (uint64_t)n_range * gpc;
-  if (finish && blockIdx.x == 0 && threadIdx.x == 0) {   // the Alg. 3 kernels run after this graph node
-    D.n_hits[0] = 0;
-    D.n_hits[1] = 0;   // result-block slot for the chain count (written by k_union)
-  }
+  if (finish && blockIdx.x == 0) zero_detect_counters(D, cs_lo, n_range);
   const uint64_t n_warps = ((uint64_t)gridDim.x * kDetThreads) >> 5;
   for (uint64_t gi = ((uint64_t)blockIdx.x * kDetThreads + threadIdx.x) >> 5; gi < total; gi += n_warps) {
     const uint32_t cs = cs_lo + (uint32_t)(gi / gpc);
@@ -496,15 +497,13 @@ __global__ void __launch_bounds__(kDetThreads) k_zero_counts(const __grid_consta
       }
     }
     // lane k ends up holding the population of column c0 + k (transpose-reduce of 16 warp sums)
-    uint32_t mine = 0, zsum = 0;
+    uint32_t mine = 0;
 #pragma unroll
     for (uint32_t k = 0; k < kGroup; ++k) {
       const uint32_t t = warp_sum(pop[k]);
       if (lane == (int)k) mine = t;
-      if (c0 + k < c1) zsum += G.g - t;
     }
     if (lane < (int)(c1 - c0)) D.zc[(size_t)cs * G.ra_cols + G.ra_off[i] + c0 + lane] = G.g - mine;
-    if (finish && i == 0 && lane == 0) atomicAdd(D.ztot + cs, (unsigned long long)zsum);
   }
 }
 
@@ -520,15 +519,28 @@ __global__ void __launch_bounds__(kDetThreads) k_hot(const __grid_constant__ Geo
   const uint32_t cs = cs_lo + blockIdx.x / G.num_ra;
   const uint32_t a = blockIdx.x % G.num_ra;
   cbaa_cs_stats* rec = D.rec + cs;
+  // Ztot = zero bits of RA(0) of this CS (η source, Q12): every CTA of the CS sums the same c(0) counts
+  __shared__ unsigned long long s_zsum[kDetWarps];
+  unsigned long long zpart = 0;
+  const uint32_t* z0 = D.zc + (size_t)cs * G.ra_cols;   // RA(0) block
+  for (uint32_t c = threadIdx.x; c < G.ncols[0]; c += kDetThreads) zpart += __ldcg(z0 + c);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zpart += __shfl_xor_sync(0xffffffffu, zpart, o);
+  if ((threadIdx.x & 31) == 0) s_zsum[threadIdx.x >> 5] = zpart;
+  __syncthreads();
   if (threadIdx.x == 0) {
+    unsigned long long ztot = 0;
+    for (int w = 0; w < kDetWarps; ++w) ztot += s_zsum[w];
     cbaa_cs_stats st;
-    cs_math(G, __ldcg(D.ztot + cs), theta, &st);
+    cs_math(G, ztot, theta, &st);
     if (a == 0) {
       rec->ztot = st.ztot;
       rec->eta = st.eta;
       rec->eps = st.eps;
       rec->theta_bn = st.theta_bn;
       rec->zmax = st.zmax;
+      rec->candidates = 0;   // accumulated by the Alg. 3 kernels, which run after this grid
+      rec->hits = 0;
     }
     s_zmax = st.zmax;
   }
