@@ -41,6 +41,7 @@ struct cbaa_handle {
   uint32_t passes = 1;
   uint32_t* cube = nullptr;
   bool cube_external = false;   // cube memory owned by the caller (cbaa_create_ext)
+  uint32_t* prefix_bits = nullptr;   // a0 classifier bitmaps (direction = inner prefix)
   uint64_t cube_bytes = 0;
   uint64_t cube_words = 0;
   // detect scratch (one allocation, see alloc_scratch)
@@ -150,6 +151,10 @@ int validate(const cbaa_config* c, std::string* why) {
   if (c->direction != CBAA_DIR_NORMALIZED && c->direction != CBAA_DIR_INNER_PREFIX)
     return bad("direction must be CBAA_DIR_NORMALIZED or CBAA_DIR_INNER_PREFIX");
   if (c->n_prefixes > CBAA_MAX_PREFIXES) return bad("at most 16 inner prefixes");
+  for (uint32_t k = 0; k < c->n_prefixes && k < CBAA_MAX_PREFIXES; ++k) {
+    const uint32_t m = c->inner_mask[k];
+    if ((~m) & ((~m) + 1u)) return bad("inner_mask must be a CIDR mask (leading ones, then zeros)");
+  }
   if (c->update_mode != CBAA_UPDATE_TEST_SET && c->update_mode != CBAA_UPDATE_RED)
     return bad("update_mode must be CBAA_UPDATE_TEST_SET or CBAA_UPDATE_RED");
   uint64_t csb = 0;
@@ -277,6 +282,31 @@ int alloc_scratch(cbaa_handle* h) {
   h->h_hits_cap = 4096;
   CK(h, cudaMallocHost(&h->h_res, 64 + h->h_hits_cap * sizeof(cbaa_host)));
   h->h_hits = (cbaa_host*)((char*)h->h_res + 64);
+  return CBAA_OK;
+}
+
+// The a0 classifier's two 65536-bit maps over the top 16 address bits (see Geo::full_bits).
+int upload_prefix_bits(cbaa_handle* h) {
+  std::vector<uint32_t> bits(2 * 2048, 0);
+  uint32_t* full = bits.data();
+  uint32_t* part = bits.data() + 2048;
+  for (uint32_t k = 0; k < h->cfg.n_prefixes; ++k) {
+    const uint32_t m = h->cfg.inner_mask[k], pre = h->cfg.inner_prefix[k] & m;
+    const uint32_t len = (uint32_t)__builtin_popcount(m);
+    if (len <= 16) {   // covers whole top-16 buckets
+      const uint32_t lo = pre >> 16, cnt = 1u << (16 - len);
+      for (uint32_t t = lo; t < lo + cnt; ++t) full[t >> 5] |= 1u << (t & 31);
+    } else {
+      const uint32_t t = pre >> 16;
+      part[t >> 5] |= 1u << (t & 31);
+    }
+  }
+  void* d = nullptr;
+  CK(h, cudaMalloc(&d, bits.size() * 4));
+  CK(h, cudaMemcpy(d, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+  h->prefix_bits = (uint32_t*)d;
+  h->G.full_bits = h->prefix_bits;
+  h->G.part_bits = h->prefix_bits + 2048;
   return CBAA_OK;
 }
 
@@ -459,6 +489,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemset(cube)");
   }
   if (!rc) rc = alloc_scratch(h);
+  if (!rc && cfg->direction == CBAA_DIR_INNER_PREFIX) rc = upload_prefix_bits(h);
   if (rc) {
     std::fprintf(stderr, "cbaa_create: %s\n", h->err.c_str());
     cbaa_destroy(h);
@@ -494,6 +525,7 @@ void cbaa_destroy(cbaa_handle* h) {
   DeviceGuard dg(h->device);
   if (h->cube && !h->cube_external) cudaFree(h->cube);
   if (h->scratch) cudaFree(h->scratch);
+  if (h->prefix_bits) cudaFree(h->prefix_bits);
   if (h->D.cand) cudaFree(h->D.cand);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   if (h->h_cnt) cudaFreeHost(h->h_cnt);

@@ -27,6 +27,11 @@ struct Geo {
   int32_t direction, theta_formula;
   uint32_t n_prefix;
   uint32_t prefix[CBAA_MAX_PREFIXES], pmask[CBAA_MAX_PREFIXES];
+  // inner-prefix classification by the top 16 address bits: bit t of full_bits set ⇔ every address with
+  // top-16 value t is inner (prefixes /0-/16); bit t of part_bits set ⇔ some are (longer prefixes,
+  // exact check).  Device pointers to 2 × 2048 words owned by the handle; null if direction = normalised.
+  const uint32_t* full_bits;
+  const uint32_t* part_bits;
   uint64_t tuple_cap;
 };
 

@@ -41,7 +41,12 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
   return v;
 }
 
+// a0 membership test: one L1-resident bitmap probe by the top 16 bits; only addresses in a /16 that holds
+// a longer prefix fall through to the exact comparison against the prefix list.
 __device__ __forceinline__ bool is_inner(const Geo& G, uint32_t ip) {
+  const uint32_t t = ip >> 16;
+  if ((__ldg(G.full_bits + (t >> 5)) >> (t & 31)) & 1u) return true;
+  if (!((__ldg(G.part_bits + (t >> 5)) >> (t & 31)) & 1u)) return false;
   bool in = false;
   for (uint32_t k = 0; k < G.n_prefix; ++k) in |= (ip & G.pmask[k]) == G.prefix[k];
   return in;
