@@ -1,4 +1,5 @@
-"""Update time vs address-range passes for large cubes (C5 window, 500M pairs)."""
+"""Update time vs address-range passes for large cubes (C5-shaped window).
+Usage: python tools/passes_perf.py "r,g,cbn;r,g,cbn" "1,2,4" [n_pairs]"""
 import json
 import os
 import sys
@@ -15,13 +16,16 @@ def main():
     from oracle import oracle as O   # geometry dicts only
     from paper_1901_06207_b200 import workload as W
     from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
-    w = W.generate(W.c5_spec(), 5, with_raw=False)
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 500_000_000
+    w = W.generate(W.c5_spec(n=n), 5, with_raw=False)
     src = torch.from_numpy(w.src.view(np.int32)).cuda()
     dst = torch.from_numpy(w.dst.view(np.int32)).cuda()
     del w
-    geos = [g for g in W.c5_geometries() if (g["r"], g["g"], g["cbn"][0]) in ((4, 4096, 14), (6, 4096, 12), (6, 8192, 14), (4, 4096, 12))]
+    sel = [(int(x.split(",")[0]), int(x.split(",")[1]), int(x.split(",")[2])) for x in sys.argv[1].split(";")]
+    plist = [int(x) for x in sys.argv[2].split(",")]
+    geos = [g for g in W.c5_geometries() if (g["r"], g["g"], g["cbn"][0]) in sel]
     for geo in geos:
-        for passes in (1, 2, 3, 4, 6, 8, 12):
+        for passes in plist:
             cb = Cbaa(config_from_dict(dict(O.default_params(), update_passes=passes, **geo)), 0)
             ts = []
             for k in range(5):
@@ -33,7 +37,7 @@ def main():
                 torch.cuda.synchronize()
                 if k >= 1:
                     ts.append(a.elapsed_time(b))
-            print(json.dumps({"r": geo["r"], "g": geo["g"], "cbn": geo["cbn"][0], "cube_mib": cb.nbytes >> 20,
+            print(json.dumps({"n": n, "r": geo["r"], "g": geo["g"], "cbn": geo["cbn"][0], "cube_mib": cb.nbytes >> 20,
                               "passes": passes, "update_ms": round(sorted(ts)[len(ts) // 2], 3)}), flush=True)
             cb.close()
             torch.cuda.empty_cache()
