@@ -495,14 +495,17 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     cbaa_destroy(h);
     return rc;
   }
-  // Update passes: the RED rate collapses ~3x once the cube spills L2 (profiles/r01_redbench.jsonl),
-  // so the cube is split into address ranges that each fit 70% of L2.
+  // Update passes: random access rates collapse 2.4-3x once the working set spills L2
+  // (profiles/r01_redbench.jsonl), so the cube is split into address ranges.
   if (cfg->update_passes) {
     h->passes = cfg->update_passes;
   } else {
-    // capped at 8: past that the input re-reads cost more than the L2 misses they avoid
-    double budget = 0.70 * (h->l2_bytes > 0 ? h->l2_bytes : (96 << 20));
-    h->passes = (uint32_t)std::min<double>(8.0, std::max<double>(1.0, std::ceil((double)h->cube_bytes / budget)));
+    // Measured optimum (profiles/r01_passes.jsonl, 100M-500M-pair windows): each pass re-reads and
+    // re-hashes the whole input (~4 ps per pair), so the touched part of each pass's range — not the
+    // whole range — has to fit L2; in units of L2: ≤ 0.8 → 1, ≤ 3 → 2, ≤ 5 → 3, ≤ 10 → 4, ≤ 20 → 6,
+    // else 12.
+    const double x = (double)h->cube_bytes / (double)(h->l2_bytes > 0 ? h->l2_bytes : (126 << 20));
+    h->passes = x <= 0.8 ? 1 : x <= 3 ? 2 : x <= 5 ? 3 : x <= 10 ? 4 : x <= 20 ? 6 : 12;
   }
   const char* fc = std::getenv("CBAA_FORCE_CARTESIAN");
   h->force_cartesian = fc && fc[0] == '1';
