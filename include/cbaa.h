@@ -60,6 +60,7 @@ extern "C" {
 /* How the update kernel sets a bit; the resulting cube is identical (bits only go 0 -> 1). */
 #define CBAA_UPDATE_TEST_SET 0  /* L1-cached load of the word; RED.OR only if the bit is still 0 (default) */
 #define CBAA_UPDATE_RED 1       /* unconditional RED.OR per bit: the paper's write-only update   */
+#define CBAA_UPDATE_BINNED 2    /* pairs binned by (CS, row group) and applied in shared memory (large n) */
 
 #define CBAA_DIR_NORMALIZED 0   /* src = inner, dst = outer as given (Q25)                 */
 #define CBAA_DIR_INNER_PREFIX 1 /* classify by inner prefixes; swap or skip              */
@@ -95,7 +96,9 @@ typedef struct {
   uint32_t detect_overlap;             /* 1: detect will run beside another handle's update (pipelined    */
                                        /* windows): window-end kernels use no shared memory so they fit   */
                                        /* next to the update's CTAs; 0: fastest standalone detect (TMA)   */
-  uint32_t reserved[3];
+  uint32_t bin_min_pairs;              /* CBAA_UPDATE_BINNED: calls with fewer pairs take the direct      */
+                                       /* kernel (0 = auto: max(2^20, cube words / 4))                    */
+  uint32_t reserved[2];
 } cbaa_config;
 
 /* One restored super host (Alg. 3 output). */
@@ -159,7 +162,12 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
  * host-order IPv4 (src = inner, dst = outer unless direction = INNER_PREFIX).
  * Sets |RA|+|VA| bits per pair with 32-bit atomic OR (Q11); with the default
  * update_mode the word is loaded first and only a missing bit is ORed in — the
- * cube is identical either way.  Updates accumulate until cbaa_reset; calls on
+ * cube is identical either way.  With CBAA_UPDATE_BINNED and n above the
+ * handle's threshold the pairs are first binned by (CS, row group) into a
+ * device scratch of 4 B per pair (≤ 2^28 pairs per chunk, allocated on first
+ * use) and the bits are set in shared memory, then OR-ed into the cube; below
+ * the threshold, or for geometries whose tables do not fit, the call takes the
+ * test-and-set kernel.  Updates accumulate until cbaa_reset; calls on
  * one handle must be stream-ordered with its detect/merge/reset.  Any 4-byte
  * alignment is accepted (16-B aligned arrays take the vector path).  Async on
  * stream. */

@@ -21,7 +21,7 @@ OK = 0
 E_CONFIG, E_ARG, E_CUDA, E_MISMATCH, E_CAPACITY, E_TUPLE_CAP, E_NOMEM = -1, -2, -3, -4, -5, -6, -7
 THETA_PAPER, THETA_INVERTED = 0, 1
 DIR_NORMALIZED, DIR_INNER_PREFIX = 0, 1
-UPDATE_TEST_SET, UPDATE_RED = 0, 1
+UPDATE_TEST_SET, UPDATE_RED, UPDATE_BINNED = 0, 1, 2
 SKETCH_REPLACE, SKETCH_MERGE = 0, 1
 
 
@@ -36,7 +36,7 @@ class Config(C.Structure):
         ("n_prefixes", C.c_uint32), ("inner_prefix", C.c_uint32 * MAX_PREFIXES),
         ("inner_mask", C.c_uint32 * MAX_PREFIXES), ("update_passes", C.c_uint32), ("hit_capacity", C.c_uint32),
         ("update_mode", C.c_uint32), ("join_capacity", C.c_uint32), ("detect_overlap", C.c_uint32),
-        ("reserved", C.c_uint32 * 3),
+        ("bin_min_pairs", C.c_uint32), ("reserved", C.c_uint32 * 2),
     ]
 
     def to_dict(self) -> dict:
@@ -154,6 +154,7 @@ def config_from_dict(p: dict) -> Config:
     c.update_mode = p.get("update_mode", UPDATE_TEST_SET)
     c.join_capacity = p.get("join_capacity", 0)
     c.detect_overlap = p.get("detect_overlap", 0)
+    c.bin_min_pairs = p.get("bin_min_pairs", 0)
     return c
 
 

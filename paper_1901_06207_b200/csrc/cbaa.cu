@@ -17,6 +17,7 @@
 #include "cbaa.h"
 #include "geometry.cuh"
 #include "kernels.cuh"
+#include "binned.cuh"
 
 using namespace cbaa;
 
@@ -71,6 +72,15 @@ struct cbaa_handle {
   DetectKey graph_key{};
   int graph_kernels = 0;
   int use_join = 0;          // |RA| = 3 and not forced Cartesian
+  // binned update (CBAA_UPDATE_BINNED, binned.cuh)
+  BinGeo B{};
+  int binnable = 0;          // geometry fits the binned kernels' shared-memory tables
+  uint64_t bin_min = 0;      // fewer pairs per call than this take the direct kernel
+  uint64_t bin_chunk = 1ull << 28;   // pairs per count/scatter/apply round (CBAA_BIN_CHUNK, tests)
+  uint32_t* bin_ent = nullptr;
+  uint64_t bin_cap = 0;
+  uint32_t* bin_offs = nullptr;   // [nbins · nblk + 1]
+  uint32_t* bin_part = nullptr;
   std::string err;
 };
 
@@ -155,8 +165,9 @@ int validate(const cbaa_config* c, std::string* why) {
     const uint32_t m = c->inner_mask[k];
     if ((~m) & ((~m) + 1u)) return bad("inner_mask must be a CIDR mask (leading ones, then zeros)");
   }
-  if (c->update_mode != CBAA_UPDATE_TEST_SET && c->update_mode != CBAA_UPDATE_RED)
-    return bad("update_mode must be CBAA_UPDATE_TEST_SET or CBAA_UPDATE_RED");
+  if (c->update_mode != CBAA_UPDATE_TEST_SET && c->update_mode != CBAA_UPDATE_RED &&
+      c->update_mode != CBAA_UPDATE_BINNED)
+    return bad("update_mode must be CBAA_UPDATE_TEST_SET, CBAA_UPDATE_RED or CBAA_UPDATE_BINNED");
   uint64_t csb = 0;
   for (uint32_t a = 0; a < c->num_ra + c->num_va; ++a) csb += ((uint64_t)1 << c->cbn[a]) * c->g;
   if ((csb << c->r) / 8 > (16ull << 30) - 16) return bad("cube must be smaller than 16 GiB");
@@ -388,7 +399,58 @@ int launch_update_aos(cbaa_handle* h, const uint32_t* pairs, uint64_t n, uint32_
   return launch_check(h, "k_update_aos");
 }
 
+// Binned update (binned.cuh): count → scan → scatter → apply, in chunks of at most 2^28 pairs.
+int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
+  const uint64_t kChunk = h->bin_chunk;
+  const BinGeo& B = h->B;
+  const uint64_t m_cnt = (uint64_t)B.nbins * B.nblk;
+  const uint32_t n_part = (uint32_t)((m_cnt + kScanSeg - 1) / kScanSeg);
+  const uint64_t want = std::min(n, kChunk);
+  if (h->bin_cap < want) {
+    if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
+    h->bin_ent = nullptr;
+    h->bin_cap = 0;
+    CK(h, cudaMalloc(&h->bin_ent, want * 4));
+    h->bin_cap = want;
+  }
+  if (!h->bin_offs) {
+    CK(h, cudaMalloc(&h->bin_offs, (m_cnt + 1) * 4));
+    CK(h, cudaMalloc(&h->bin_part, (uint64_t)n_part * 4));
+  }
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  const size_t sm_cnt = (size_t)B.nbins * 4;
+  const size_t sm_sc = (size_t)(2 * B.nbins + 1) * 4 + (size_t)kBinTile * 6;
+  const size_t sm_ap = (size_t)B.ncols * 4;
+  const uint32_t n_wg = h->G.n_cs * h->G.wpc;
+  for (uint64_t off = 0; off < n; off += kChunk) {
+    const uint64_t m = std::min(kChunk, n - off);
+    const uint32_t* a = src + off;
+    const uint32_t* b = dst + off;
+    const uint64_t per = (((m + B.nblk - 1) / B.nblk) + 3) & ~3ull;
+    const int vec = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
+    if (prefix) k_bin_count<true><<<B.nblk, kBinThreads, sm_cnt, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->skipped);
+    else k_bin_count<false><<<B.nblk, kBinThreads, sm_cnt, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, nullptr);
+    int rc = launch_check(h, "k_bin_count");
+    if (rc) return rc;
+    k_bin_scan_reduce<<<n_part, kBinThreads, 0, s>>>(h->bin_offs, m_cnt, h->bin_part);
+    if ((rc = launch_check(h, "k_bin_scan_reduce"))) return rc;
+    k_bin_scan_down<<<n_part, kBinThreads, 0, s>>>(h->bin_offs, m_cnt, h->bin_part);
+    if ((rc = launch_check(h, "k_bin_scan_down"))) return rc;
+    if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->bin_ent);
+    else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->bin_ent);
+    if ((rc = launch_check(h, "k_bin_scatter"))) return rc;
+    if (h->G.num_ra == 3 && h->G.num_va == 1)
+      k_bin_apply<3, 1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, h->bin_offs, h->bin_ent, h->cube);
+    else
+      k_bin_apply<0, 0><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, h->bin_offs, h->bin_ent, h->cube);
+    if ((rc = launch_check(h, "k_bin_apply"))) return rc;
+  }
+  return CBAA_OK;
+}
+
 int update_all_passes(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
+  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min)
+    return update_binned(h, src, dst, n, s);
   const uint64_t W = h->cube_words;
   for (uint32_t p = 0; p < h->passes; ++p) {
     uint64_t lo = W * p / h->passes, hi = W * (p + 1) / h->passes;
@@ -512,6 +574,33 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
   h->use_join = h->G.num_ra == 3 && !h->force_cartesian;
   const char* nt = std::getenv("CBAA_NO_TMA");
   h->no_tma = nt && nt[0] == '1';
+  {   // binned update geometry (binned.cuh): bins (cs, row >> s), word groups of Σc(i) words
+    BinGeo& B = h->B;
+    B.s = std::min<uint32_t>(5, cfg->r);
+    uint32_t lg = 0;
+    while ((1u << lg) < cfg->g) ++lg;
+    B.bpc_log2 = lg - B.s;
+    B.nbins = h->G.n_cs << B.bpc_log2;
+    B.nblk = (uint32_t)h->sms * 2;
+    B.ncols = h->G.cs_words / h->G.wpc;
+    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;
+    const char* bm = std::getenv("CBAA_BIN_MIN");
+    h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
+                 : bm                 ? std::strtoull(bm, nullptr, 10)
+                                      : std::max<uint64_t>(1u << 20, h->cube_words / 4);
+    const char* bc = std::getenv("CBAA_BIN_CHUNK");
+    if (bc && std::strtoull(bc, nullptr, 10) > 0)
+      h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
+    if (h->binnable) {
+      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)(2 * B.nbins + 1) * 4 + kBinTile * 6, sm_ap = (int)B.ncols * 4;
+      cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_apply<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+    }
+  }
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<3, 1, CBAA_UPDATE_TEST_SET, false>, kThreads, 0);
   h->upd_blocks = std::max(1, occ);
@@ -528,6 +617,9 @@ void cbaa_destroy(cbaa_handle* h) {
   DeviceGuard dg(h->device);
   if (h->cube && !h->cube_external) cudaFree(h->cube);
   if (h->scratch) cudaFree(h->scratch);
+  if (h->bin_ent) cudaFree(h->bin_ent);
+  if (h->bin_offs) cudaFree(h->bin_offs);
+  if (h->bin_part) cudaFree(h->bin_part);
   if (h->prefix_bits) cudaFree(h->prefix_bits);
   if (h->D.cand) cudaFree(h->D.cand);
   if (h->h_rec) cudaFreeHost(h->h_rec);

@@ -455,3 +455,119 @@ def test_update_interleaved_pairs(paper, n, off, mode):
     cb.update_pairs(t)
     ref, _ = O.update(paper, src, dst)
     assert np.array_equal(gpu_cube(cb), ref)
+
+
+# ------------------------------------------------------------------ binned update (CBAA_UPDATE_BINNED)
+BIN = dict(update_mode=2, bin_min_pairs=1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 1023, 8191, 8192, 8193, 300_001])
+def test_binned_small_and_ragged(paper, n):
+    """Count → scan → scatter → apply on ragged sizes: partial scatter tiles, CTAs with empty chunks."""
+    src, dst = W.random_pairs(n, 70 + n)
+    cb = handle(paper, **BIN)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_binned_random_geometries(seed):
+    """Entry row bits s = min(5, r) for r = 1..8, 2-4 RAs, 0-2 VAs, g = 32..256, full detection."""
+    p = random_params(200 + seed, max_cube_bytes=1 << 24)
+    spec = W.WindowSpec(n=200_000, n_hosts=3000, n_flows=30000, scanners=(300, 600, 900), victims=(500,))
+    w = W.generate(spec, 300 + seed)
+    full_check(p, w.src, w.dst, theta=max(8, p["g"] // 2), **BIN)
+
+
+@pytest.mark.parametrize("off_s, off_d", [(1, 1), (0, 3), (2, 1)])
+def test_binned_misaligned(paper, off_s, off_d):
+    src, dst = W.random_pairs(40_000, 12)
+    big_s = dev(np.concatenate([np.zeros(4, np.uint32), src]))
+    big_d = dev(np.concatenate([np.zeros(4, np.uint32), dst]))
+    n = 39_001
+    cb = handle(paper, **BIN)
+    cb.reset()
+    cb.update(big_s[off_s: off_s + n], big_d[off_d: off_d + n])
+    ref, _ = O.update(paper, big_s.cpu().numpy().view(np.uint32)[off_s: off_s + n],
+                      big_d.cpu().numpy().view(np.uint32)[off_d: off_d + n])
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+def test_binned_hot_spot_and_skew(paper):
+    """One word hammered by every pair; one host with 90 % of the packets (one CS's bins take almost
+    everything); a lone host with 50K distinct peers, detected like the oracle."""
+    n = 400_000
+    src = np.full(n, 0x0A000001, np.uint32)
+    dst = np.full(n, 0x08080808, np.uint32)
+    cb = handle(paper, **BIN)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src[:1], dst[:1])
+    assert np.array_equal(gpu_cube(cb), ref)
+    s2, d2 = W.random_pairs(n, 13)
+    s2[: 9 * n // 10] = 0x0A000002
+    cb.reset()
+    cb.update(dev(s2), dev(d2))
+    ref, _ = O.update(paper, s2, d2)
+    assert np.array_equal(gpu_cube(cb), ref)
+    dst3 = np.arange(n, dtype=np.uint32) % 50_000 + 0x20000000
+    full_check(paper, src, dst3, 1024, **BIN)
+
+
+def test_binned_inner_prefix(paper):
+    """a0 in the binned kernels: both count and scatter classify; skips are counted once."""
+    spec = W.WindowSpec(n=300_000, n_hosts=5000, n_flows=40000, victims=(3000,), scanners=(2500,))
+    w = W.generate(spec, 4)
+    q = dict(paper, direction=1, prefixes=w.prefixes, **BIN)
+    junk_s, junk_d = W.random_pairs(1000, 9)
+    raw_s = np.concatenate([w.raw_src, junk_s])
+    raw_d = np.concatenate([w.raw_dst, junk_d])
+    cb = handle(q)
+    cb.reset()
+    cb.update(dev(raw_s), dev(raw_d))
+    ref, skipped = O.update(q, raw_s, raw_d)
+    assert np.array_equal(gpu_cube(cb), ref)
+    assert cb.skipped() == skipped >= 1000
+
+
+def test_binned_chunks_and_accumulate(paper, monkeypatch):
+    """Several count/scatter/apply rounds per call (small CBAA_BIN_CHUNK) and across calls, OR-ed into a
+    cube that already holds bits from the direct kernel."""
+    monkeypatch.setenv("CBAA_BIN_CHUNK", "100003")
+    a_s, a_d = W.random_pairs(350_000, 21)
+    b_s, b_d = W.random_pairs(50_000, 22)
+    cb = handle(paper, update_mode=2, bin_min_pairs=100_000)
+    cb.reset()
+    cb.update(dev(b_s), dev(b_d))         # below bin_min_pairs: direct kernel
+    cb.update(dev(a_s), dev(a_d))         # 4 binned rounds
+    ref, _ = O.update(paper, np.concatenate([a_s, b_s]), np.concatenate([a_d, b_d]))
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("r, g, cbn", [(6, 4096, 12), (2, 1024, 10), (4, 4096, 14), (0, 64, 11), (2, 1024, 15)])
+def test_binned_shapes(r, g, cbn):
+    """r ≥ 5 (s = 5, one bin per word group), r = 2 (s = 2, 8 bins per group), r = 0 (s = 0, the entry
+    is the whole mangled IP), and column counts too large for the shared-memory word group (fallback to
+    the direct kernel) — all bit-exact."""
+    L = 32 - r
+    clbs = [0, L // 3, 2 * L // 3]
+    ep = [clbs[1] - clbs[0], clbs[2] - clbs[1], L - clbs[2]]
+    p = O.default_params()
+    p.update(r=r, g=g, clbs=clbs, cbn=[max(ep[i], min(cbn, ep[i] + ep[(i + 1) % 3])) for i in range(3)] + [min(cbn, 14)])
+    assert O.validate(p)[0] == 0, (p, O.validate(p))
+    src, dst = W.random_pairs(200_000, 31 + r)
+    cb = handle(p, **BIN)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(p, src, dst)
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.slow
+def test_binned_c2_full_size(paper):
+    """Config 2 at full size through the binned kernels (default threshold, the bench configuration)."""
+    w = W.generate(W.C2, 1, with_raw=False)
+    cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024, update_mode=2)
+    assert 550 <= len(hosts) <= 750
