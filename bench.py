@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
-    ap.add_argument("--update-mode", choices=["test_set", "red"], default="test_set")
+    ap.add_argument("--update-mode", choices=["test_set", "red", "binned"], default="binned",
+                    help="binned (default): count/scatter/apply through shared memory; test_set / red: the "
+                         "direct random-access kernel (DESIGN.md §6)")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N=1: run windows strictly one after another (default: window k's detect overlaps "
                          "window k+1's reset+update on a second cube and a high-priority stream)")
@@ -152,6 +154,14 @@ def ncu_traffic():
         return None
 
 
+def ncu_binned():
+    """DRAM bytes per launch of the binned-update kernels from the committed ncu --set full capture."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_binned.json")))
+    except Exception:
+        return {}
+
+
 def ncu_update_counters():
     """Per-launch L1/L2 utilisation of k_update from the committed ncu --set full capture."""
     try:
@@ -236,14 +246,14 @@ def main():
         backend = os.environ.get("CBAA_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
     torch.cuda.set_device(local)
-    peaks_acc = access_peaks() if rank == 0 else {}
+    peaks_acc = access_peaks() if rank == 0 and args.update_mode != "binned" else {}
     spec, w = workload(args.workload, args.seed, rank, world)
     n = spec.n
     src = torch.from_numpy(w.src.view(np.int32)).cuda()
     dst = torch.from_numpy(w.dst.view(np.int32)).cuda()
     cfg = default_config()
     cfg.update_passes = args.passes
-    cfg.update_mode = 0 if args.update_mode == "test_set" else 1
+    cfg.update_mode = {"test_set": 0, "red": 1, "binned": 2}[args.update_mode]
     from paper_1901_06207_b200.cbaa import cube_bytes
     peer = None
     exchange = args.exchange if world > 1 else "none"
@@ -305,6 +315,7 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = cb.kernel_launches
+    cb.set_phase_timing(True)       # event pair around every update kernel, on its stream
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -317,6 +328,8 @@ def main():
     if world > 1:
         dist.barrier()
     launches = cb.kernel_launches - launches0
+    phase_ms, phase_calls = cb.update_phase_ms()
+    cb.set_phase_timing(False)
     elapsed_ms = t_start.elapsed_time(t_end)
     upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
     post_ms = [e[1].elapsed_time(e[2]) for e in evs]
@@ -379,6 +392,8 @@ def main():
         run_pipelined(max(args.warmup, 3))
         torch.cuda.synchronize()
         launches0 = cbs[0].kernel_launches + cb2.kernel_launches
+        for c in cbs:
+            c.set_phase_timing(True)
         pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
         p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
@@ -392,6 +407,12 @@ def main():
         if world > 1:
             dist.barrier()
         launches = cbs[0].kernel_launches + cb2.kernel_launches - launches0
+        phase_ms, phase_calls = [0.0] * 4, 0
+        for c in cbs:
+            ms_c, calls_c = c.update_phase_ms()
+            phase_ms = [a + b for a, b in zip(phase_ms, ms_c)]
+            phase_calls += calls_c
+            c.set_phase_timing(False)
         elapsed_ms = p_start.elapsed_time(p_end)
         if world > 1:
             elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
@@ -444,27 +465,53 @@ def main():
     value = n * world * args.steps / (elapsed_ms / 1e3)
     upd = statistics.median(upd_ms)
     passes = cb.update_passes
-    algo = 4 * n                       # |RA|+|VA| = 4 bit-sets per pair, one random word each
-    achieved = algo / (upd / 1e3)
-    peak_acc = max(peaks_acc.values()) if peaks_acc else None
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
-    traffic = ncu_traffic()
-    roofline = {"kernel": "k_update (cbaa_update, all passes)", "bound": "lsu_random_word",
-                "achieved": achieved / 1e9, "peak": (peak_acc or float("nan")) / 1e9, "unit": "G word-updates/s",
-                "frac": achieved / peak_acc if peak_acc else None,
-                "traffic": (traffic or {}).get("dram_bytes_per_update"),
-                "algorithmic": f"4 random 32-bit word updates per pair (one per RA/VA bit, Alg. 1) x {n} pairs "
-                               f"per update; {passes} address-range launches",
-                "peak_source": "tools/redbench --quick in this run: best of random 32-bit LDG (L2 / L1-cached) and "
-                               "RED.OR over a 64 MiB L2-resident buffer (not in MEASURED_PEAKS.json)",
-                "peak_ldg": peaks_acc.get("ldg", 0) / 1e9, "peak_ldg_ca": peaks_acc.get("ldg_ca", 0) / 1e9,
-                "peak_red": peaks_acc.get("red", 0) / 1e9,
-                "update_ms": upd, "launch_ms": upd / passes, "update_passes": passes,
-                "update_mode": args.update_mode, "ncu_per_pass": ncu_update_counters()}
-    roofline_hbm = {"bound": "hbm", "achieved": 8 * n / (upd / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                    "frac": 8 * n / (upd / 1e3) / 1e9 / hbm,
-                    "note": "input stream, 8 B/pair algorithmic; peak = MEASURED_PEAKS.json hbm_gbs"}
+    per_call = [t / max(1, phase_calls) for t in phase_ms]
+    binned = args.update_mode == "binned"
+    if binned:
+        # binned update (binned.cuh): algorithmic DRAM bytes of each kernel per launch
+        nb = ncu_binned()
+        algo = {"k_bin_count": 8 * n, "k_bin_starts": 3 * 4 * 4096, "k_bin_scatter": 12 * n,
+                "k_bin_apply": 4 * n + cb.nbytes}
+        kernels = {}
+        for name, t in zip(algo, per_call):
+            kernels[name] = {"ms": t, "share": t / max(1e-9, sum(per_call)), "algorithmic_bytes": algo[name],
+                             "gbs": algo[name] / (t / 1e3) / 1e9 if t > 0 else None,
+                             "frac_hbm": algo[name] / (t / 1e3) / 1e9 / hbm if t > 0 else None,
+                             "ncu_dram_bytes": (nb.get(name) or {}).get("dram_bytes_per_launch")}
+        dom = max(kernels, key=lambda k: kernels[k]["ms"])
+        kd = kernels[dom]
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
+                    "frac": kd["frac_hbm"], "traffic": kd["ncu_dram_bytes"],
+                    "algorithmic": {"k_bin_count": "8 B/pair read", "k_bin_scatter": "8 B/pair read + 4 B/pair entry "
+                                    "written", "k_bin_apply": "4 B/pair entry read + the cube's words OR-ed once"},
+                    "per_launch_ms": kd["ms"], "timing": "CUDA event pair around every update kernel on its launch "
+                    "stream over the timed region (cbaa_set_phase_timing), averaged per update call",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernels": kernels,
+                    "update_ms": upd, "update_mode": args.update_mode,
+                    "traffic_source": "profiles/r01_ncu_binned.json (ncu --set full, dram__bytes_read+write)"}
+        roofline_hbm = None
+    else:
+        algo = 4 * n                       # |RA|+|VA| = 4 bit-sets per pair, one random word each
+        achieved = algo / (upd / 1e3)
+        peak_acc = max(peaks_acc.values()) if peaks_acc else None
+        traffic = ncu_traffic()
+        roofline = {"kernel": "k_update (cbaa_update, all passes)", "bound": "lsu_random_word",
+                    "achieved": achieved / 1e9, "peak": (peak_acc or float("nan")) / 1e9, "unit": "G word-updates/s",
+                    "frac": achieved / peak_acc if peak_acc else None,
+                    "traffic": (traffic or {}).get("dram_bytes_per_update"),
+                    "algorithmic": f"4 random 32-bit word updates per pair (one per RA/VA bit, Alg. 1) x {n} pairs "
+                                   f"per update; {passes} address-range launches",
+                    "peak_source": "tools/redbench --quick in this run: best of random 32-bit LDG (L2 / L1-cached) "
+                                   "and RED.OR over a 64 MiB L2-resident buffer (not in MEASURED_PEAKS.json)",
+                    "peak_ldg": peaks_acc.get("ldg", 0) / 1e9, "peak_ldg_ca": peaks_acc.get("ldg_ca", 0) / 1e9,
+                    "peak_red": peaks_acc.get("red", 0) / 1e9,
+                    "update_ms": upd, "launch_ms": per_call[0] / max(1, passes), "update_passes": passes,
+                    "update_mode": args.update_mode, "ncu_per_pass": ncu_update_counters()}
+        roofline_hbm = {"bound": "hbm", "achieved": 8 * n / (upd / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": 8 * n / (upd / 1e3) / 1e9 / hbm,
+                        "note": "input stream, 8 B/pair algorithmic; peak = MEASURED_PEAKS.json hbm_gbs"}
     line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -476,7 +523,7 @@ def main():
             "ms_per_step_serial": serial_ms / args.steps,
             "update_pairs_per_s": n * world / (upd / 1e3),
             "n_super_hosts": int(len(hosts)) if hosts is not None else None,
-            "roofline": roofline, "roofline_hbm": roofline_hbm,
+            "roofline": roofline, **({"roofline_hbm": roofline_hbm} if roofline_hbm else {}),
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e,
             "baseline_note": "paper publishes no pairs/s (BASELINE.md); its restore time is <11 ms on a Titan Xp"}
     if world == 1 and not args.no_cpu_baseline:

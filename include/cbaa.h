@@ -58,7 +58,7 @@ extern "C" {
 #define CBAA_THETA_INVERTED 1 /* θ_bn = g(1−ε)e^{−θ/g}, Theorem 2 inverted (Q15)           */
 
 /* How the update kernel sets a bit; the resulting cube is identical (bits only go 0 -> 1). */
-#define CBAA_UPDATE_TEST_SET 0  /* L1-cached load of the word; RED.OR only if the bit is still 0 (default) */
+#define CBAA_UPDATE_TEST_SET 0  /* L1-cached load of the word; RED.OR only if the bit is still 0           */
 #define CBAA_UPDATE_RED 1       /* unconditional RED.OR per bit: the paper's write-only update   */
 #define CBAA_UPDATE_BINNED 2    /* pairs binned by (CS, row group) and applied in shared memory (large n) */
 
@@ -90,7 +90,7 @@ typedef struct {
   uint32_t inner_mask[CBAA_MAX_PREFIXES]; /* ip is inner iff (ip & mask[k]) == prefix[k] for some k      */
   uint32_t update_passes;              /* address-range passes of the update (0 = auto)   */
   uint32_t hit_capacity;               /* device hit buffer entries per detect (0 = 2^20)               */
-  uint32_t update_mode;                /* CBAA_UPDATE_* (0 = CBAA_UPDATE_TEST_SET)         */
+  uint32_t update_mode;                /* CBAA_UPDATE_* (cbaa_config_default: BINNED)      */
   uint32_t join_capacity;              /* CP-chain buffer of the |RA| = 3 join (0 = 2^22); on overflow    */
                                        /* detect redoes the window with the Cartesian enumeration          */
   uint32_t detect_overlap;             /* 1: detect will run beside another handle's update (pipelined    */
@@ -295,6 +295,19 @@ uint64_t cbaa_kernel_launches(const cbaa_handle* h);
 
 /* Update passes the handle uses (resolved from update_passes = 0). */
 uint32_t cbaa_update_passes(const cbaa_handle* h);
+
+/* Per-kernel timing of the update path (bench evidence).  With enable = 1 the
+ * handle records a CUDA event pair around every update kernel it launches, on
+ * the stream that kernel is launched on.  cbaa_update_phase_ms synchronizes
+ * those events and writes the milliseconds summed per phase over all update
+ * calls since the previous query (or since enabling) into ms[0..3]:
+ *   binned path: ms[0] k_bin_count, ms[1] k_bin_starts, ms[2] k_bin_scatter,
+ *                ms[3] k_bin_apply;
+ *   direct path: ms[0] k_update (every pass), ms[1..3] = 0,
+ * and the number of update calls in *calls (nullable).  ms needs cap >= 4
+ * (CBAA_E_ARG otherwise).  Host-side bookkeeping only; kernels are unchanged. */
+int cbaa_set_phase_timing(cbaa_handle* h, int enable);
+int cbaa_update_phase_ms(cbaa_handle* h, double* ms, int cap, uint64_t* calls);
 
 const char* cbaa_strerror(int code);
 const char* cbaa_last_error(const cbaa_handle* h);

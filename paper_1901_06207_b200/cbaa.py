@@ -98,6 +98,8 @@ _SIGS = {
     "cbaa_ipc_close": (C.c_int, [_h, C.c_void_p]),
     "cbaa_kernel_launches": (C.c_uint64, [_h]),
     "cbaa_update_passes": (C.c_uint32, [_h]),
+    "cbaa_set_phase_timing": (C.c_int, [_h, C.c_int]),
+    "cbaa_update_phase_ms": (C.c_int, [_h, _P(C.c_double), C.c_int, _P(C.c_uint64)]),
     "cbaa_strerror": (C.c_char_p, [C.c_int]),
     "cbaa_last_error": (C.c_char_p, [_h]),
 }
@@ -151,7 +153,7 @@ def config_from_dict(p: dict) -> Config:
         c.inner_prefix[k], c.inner_mask[k] = pre, mask
     c.update_passes = p.get("update_passes", 0)
     c.hit_capacity = p.get("hit_capacity", 0)
-    c.update_mode = p.get("update_mode", UPDATE_TEST_SET)
+    c.update_mode = p.get("update_mode", UPDATE_BINNED)
     c.join_capacity = p.get("join_capacity", 0)
     c.detect_overlap = p.get("detect_overlap", 0)
     c.bin_min_pairs = p.get("bin_min_pairs", 0)
@@ -407,6 +409,18 @@ class Cbaa:
     @property
     def update_passes(self) -> int:
         return lib().cbaa_update_passes(self._h)
+
+    def set_phase_timing(self, enable: bool = True):
+        """Event pairs around every update kernel (cbaa_set_phase_timing)."""
+        self._check(lib().cbaa_set_phase_timing(self._h, int(enable)), "cbaa_set_phase_timing")
+
+    def update_phase_ms(self):
+        """(ms per phase summed since the last query, update calls): binned [count, starts, scatter, apply],
+        direct [k_update, 0, 0, 0] (cbaa_update_phase_ms; synchronizes the recorded events)."""
+        ms = (C.c_double * 4)()
+        calls = C.c_uint64()
+        self._check(lib().cbaa_update_phase_ms(self._h, ms, 4, C.byref(calls)), "cbaa_update_phase_ms")
+        return list(ms), calls.value
 
 
 def _wrap_device(ptr: int, nbytes: int, device: int, owner):

@@ -3,15 +3,18 @@
 // All |RA|+|VA| bits of one pair sit in the same CS (RP) and in the same row (H_bv(oip)),
 // so a pair's bits all fall in one "word group" — word w = row/32 of every column of CS cs — a set of
 // Σc(i) cube words (64 KiB at the paper geometry) that fits in shared memory.  The update then runs as
-// three streaming kernels instead of 4 random L2 accesses per pair:
-//   k_bin_count    histogram of bins (cs, row >> s) per CTA chunk               reads 8 B/pair
-//   k_bin_scan_*   exclusive scan of the (bin, CTA) counts → write offsets
-//   k_bin_scatter  tile-local counting sort, bin-contiguous runs of entries     reads 8, writes 4 B/pair
+// streaming kernels instead of 4 random L2 accesses per pair:
+//   k_bin_count    bin histogram, bins (cs, row >> s), added into global totals     reads 8 B/pair
+//   k_bin_starts   exclusive scan of the totals → bin regions, write cursors
+//   k_bin_scatter  tile-local counting sort; each bin's run of a tile is appended at that bin's global
+//                  cursor (one atomic per tile and bin), so every bin region fills front to back and L2
+//                  only ever holds one partial line per bin                     reads 8, writes 4 B/pair
 //                  entry = LP << s | (row mod 2^s), s = min(5, r) (fits 32 bits since |LP| = 32 − r)
-//   k_bin_apply    one CTA per word group: the bits are set in a shared-memory copy of the word group
+//   k_bin_apply    one CTA per word group: the bits are set in a shared-memory image of the group
 //                  (test-and-set, ATOMS.OR only when the bit is still 0), then OR-ed into the cube with
 //                  one RED per non-zero word                                      reads 4 B/pair
-// The cube is the same set of bits as the direct update's (OR is order-free): parity is bit-exact.
+// The order of entries inside a bin depends on scheduling; the cube does not: it is the same set of bits
+// as the direct update's (OR is order-free), so parity is bit-exact.
 #pragma once
 #include "kernels.cuh"
 
@@ -21,16 +24,17 @@ struct BinGeo {
   uint32_t s;          // row bits kept in an entry, min(5, r)
   uint32_t bpc_log2;   // log2(bins per CS) = log2(g) − s
   uint32_t nbins;      // 2^r · g / 2^s
-  uint32_t nblk;       // CTAs of k_bin_count / k_bin_scatter; CTA j owns pairs [j·per, (j+1)·per)
+  uint32_t nblk;       // CTAs of k_bin_scatter (two per SM); CTA j reads pairs [j·per, (j+1)·per)
   uint32_t ncols;      // Σc(i): words of one word group
 };
 
-constexpr int kBinThreads = 256;
-constexpr int kBinPPT = 32;                        // pairs per thread per scatter tile
-constexpr int kBinTile = kBinThreads * kBinPPT;    // 8192 pairs
+constexpr int kBinThreads = 256;                   // k_bin_scatter: two CTAs per SM (128 regs × 512 = the RF);
+constexpr int kBinPPT = 32;                        // one 512-thread CTA with 16K-pair tiles measured 9 % slower
+constexpr int kBinTile = kBinThreads * kBinPPT;    // 8192 pairs per tile
 constexpr int kBinRankBits = 14;                   // key = bin << 14 | rank within the tile
 constexpr int kApplyThreads = 256;
-constexpr int kScanSeg = 8192;                     // elements per CTA of the offset scan
+constexpr int kApplyUnroll = 8;                    // entries per thread in flight
+constexpr int kCountThreads = 1024;
 
 template <bool PREFIX>
 __device__ __forceinline__ bool pair_bin(const Geo& G, const BinGeo& B, uint32_t iip, uint32_t oip, uint32_t& bin,
@@ -63,23 +67,23 @@ __device__ __forceinline__ void load_quad(const uint32_t* __restrict__ src, cons
   }
 }
 
-// Phase 1: per-CTA bin histogram, written bin-major: counts[bin · nblk + cta].
+// Phase 1: bin histogram of each CTA's chunk, added into counts[bin] (zeroed by k_bin_starts).
 template <bool PREFIX>
-__global__ void __launch_bounds__(kBinThreads) k_bin_count(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
+__global__ void __launch_bounds__(kCountThreads) k_bin_count(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
                                                            const uint32_t* __restrict__ src,
                                                            const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
                                                            int vec, uint32_t* __restrict__ counts,
                                                            unsigned long long* __restrict__ skipped) {
   extern __shared__ uint32_t hist[];
-  for (uint32_t b = threadIdx.x; b < B.nbins; b += kBinThreads) hist[b] = 0;
+  for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads) hist[b] = 0;
   __syncthreads();
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   uint32_t skip = 0;
-  for (uint64_t k = c0 + 4ull * threadIdx.x; k < c1; k += 4ull * kBinThreads * 2) {
+  for (uint64_t k = c0 + 4ull * threadIdx.x; k < c1; k += 4ull * kCountThreads * 2) {
     uint32_t ss[8], dd[8];
     bool in[8];
     load_quad(src, dst, k, c1, vec, ss, dd, in);
-    load_quad(src, dst, k + 4ull * kBinThreads, c1, vec, ss + 4, dd + 4, in + 4);
+    load_quad(src, dst, k + 4ull * kCountThreads, c1, vec, ss + 4, dd + 4, in + 4);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       uint32_t bin, ent;
@@ -89,54 +93,25 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_count(const __grid_constant
     }
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < B.nbins; b += kBinThreads) counts[(uint64_t)b * B.nblk + blockIdx.x] = hist[b];
+  for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads)
+    if (hist[b]) atomicAdd(counts + b, hist[b]);
   if (PREFIX && skipped) {
     skip = warp_sum(skip);
     if ((threadIdx.x & 31) == 0 && skip) atomicAdd(skipped, (unsigned long long)skip);
   }
 }
 
-// Phase 2a: sum of each kScanSeg-element segment of the counts.
-__global__ void __launch_bounds__(kBinThreads) k_bin_scan_reduce(const uint32_t* __restrict__ c, uint64_t m,
-                                                                 uint32_t* __restrict__ part) {
-  const uint64_t s0 = (uint64_t)blockIdx.x * kScanSeg;
-  uint32_t v = 0;
-  for (uint32_t i = threadIdx.x; i < kScanSeg; i += kBinThreads)
-    if (s0 + i < m) v += c[s0 + i];
-  v = warp_sum(v);
-  __shared__ uint32_t s_w[kBinThreads / 32];
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kBinThreads / 32; ++w) t += s_w[w];
-    part[blockIdx.x] = t;
-  }
-}
-
-// Phase 2b: exclusive scan in place; c[m] = total.  Each CTA adds the sum of the segments before it.
-__global__ void __launch_bounds__(kBinThreads) k_bin_scan_down(uint32_t* __restrict__ c, uint64_t m,
-                                                               const uint32_t* __restrict__ part) {
-  __shared__ uint32_t seg[kScanSeg];
-  __shared__ uint32_t s_w[kBinThreads / 32];
-  __shared__ uint32_t s_base;
-  const uint64_t s0 = (uint64_t)blockIdx.x * kScanSeg;
-  uint32_t pre = 0;
-  for (uint32_t q = threadIdx.x; q < blockIdx.x; q += kBinThreads) pre += part[q];
-  pre = warp_sum(pre);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = pre;
-  for (uint32_t i = threadIdx.x; i < kScanSeg; i += kBinThreads) seg[i] = s0 + i < m ? c[s0 + i] : 0u;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kBinThreads / 32; ++w) t += s_w[w];
-    s_base = t;
-  }
-  // each thread scans 32 consecutive elements; then a block scan of the thread totals
-  constexpr int kPer = kScanSeg / kBinThreads;
+// Phase 2: start[b] = Σ_{b' < b} counts[b'], start[nbins] = total; cursor := start; counts := 0 for the
+// next round.  One CTA (nbins ≤ 16384).
+constexpr int kStartThreads = 1024;
+__global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t* __restrict__ counts,
+                                                              uint32_t* __restrict__ start,
+                                                              uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t s_w[kStartThreads / 32];
+  const uint32_t per = (nbins + kStartThreads - 1) / kStartThreads;
+  const uint32_t b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
   uint32_t loc = 0;
-#pragma unroll 8
-  for (int i = 0; i < kPer; ++i) loc += seg[threadIdx.x * kPer + i];
+  for (uint32_t b = b0; b < b1; ++b) loc += counts[b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = loc;
 #pragma unroll
@@ -144,89 +119,105 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scan_down(uint32_t* __restr
     uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  __syncthreads();
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  uint32_t run = s_base;
-  for (int w = 0; w < warp; ++w) run += s_w[w];
-  run += incl - loc;
-#pragma unroll 8
-  for (int i = 0; i < kPer; ++i) {
-    const uint32_t x = seg[threadIdx.x * kPer + i];
-    seg[threadIdx.x * kPer + i] = run;
+  uint32_t run = incl - loc, tot = 0;
+  for (int w = 0; w < kStartThreads / 32; ++w) {
+    run += w < warp ? s_w[w] : 0u;
+    tot += s_w[w];
+  }
+  for (uint32_t b = b0; b < b1; ++b) {
+    const uint32_t x = counts[b];
+    start[b] = run;
+    cursor[b] = run;
+    counts[b] = 0;
     run += x;
   }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kScanSeg; i += kBinThreads)
-    if (s0 + i < m) c[s0 + i] = seg[i];
-  if (s0 + kScanSeg >= m && threadIdx.x == kBinThreads - 1) c[m] = run;   // last CTA: the total
+  if (threadIdx.x == 0) start[nbins] = tot;
 }
 
 // Phase 3: entries of CTA j's chunk, tile by tile: rank within the tile by ATOMS on the tile's bin
-// counts, a block scan of those counts, a shared-memory counting sort, then bin-contiguous runs written
-// at the CTA's running offset of each bin.
+// counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
+// shared-memory counting sort, then the runs written out.
 template <bool PREFIX>
-__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const __grid_constant__ Geo G,
+__global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ src,
                                                              const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
-                                                             int vec, const uint32_t* __restrict__ offs,
+                                                             int vec, uint32_t* __restrict__ cursor,
                                                              uint32_t* __restrict__ entries) {
   extern __shared__ uint32_t sm[];
-  uint32_t* base = sm;                                   // [nbins] next write offset of each bin
+  uint32_t* base = sm;                                   // [nbins] this tile's reserved slot of each bin
   uint32_t* toff = base + B.nbins;                       // [nbins + 1] tile counts → exclusive offsets
   uint32_t* stage = toff + B.nbins + 1;                  // [kBinTile] entries sorted by bin
   uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kBinTile);   // [kBinTile] their bins
   __shared__ uint32_t s_w[kBinThreads / 32];
   const uint32_t tid = threadIdx.x;
-  for (uint32_t b = tid; b < B.nbins; b += kBinThreads) {
-    base[b] = offs[(uint64_t)b * B.nblk + blockIdx.x];
-    toff[b] = 0;
-  }
+  for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
-  const uint32_t per_thr = (B.nbins + kBinThreads - 1) / kBinThreads;   // bins scanned per thread
+  const uint32_t wchunk = (B.nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
+    // all kBinPPT pairs of the thread are loaded before any is hashed (one DRAM latency per tile), then
+    // each pair's registers are reused for its key (bin, rank in the tile) and entry
     uint32_t key[kBinPPT], ent[kBinPPT];
+    bool in[kBinPPT];
 #pragma unroll
-    for (int q = 0; q < kBinPPT / 4; ++q) {
-      uint32_t ss[4], dd[4];
-      bool in[4];
-      load_quad(src, dst, t0 + 4ull * ((uint64_t)q * kBinThreads + tid), c1, vec, ss, dd, in);
+    for (int q = 0; q < kBinPPT / 4; ++q)
+      load_quad(src, dst, t0 + 4ull * ((uint64_t)q * kBinThreads + tid), c1, vec, key + 4 * q, ent + 4 * q, in + 4 * q);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        uint32_t bin = 0, en = 0;
-        const bool ok = in[e] && pair_bin<PREFIX>(G, B, ss[e], dd[e], bin, en);
-        key[4 * q + e] = ok ? (bin << kBinRankBits) | atomicAdd(&toff[bin], 1u) : 0xffffffffu;
-        ent[4 * q + e] = en;
-      }
+    for (int i = 0; i < kBinPPT; ++i) {
+      uint32_t bin = 0, en = 0;
+      const bool ok = in[i] && pair_bin<PREFIX>(G, B, key[i], ent[i], bin, en);
+      key[i] = ok ? (bin << kBinRankBits) | atomicAdd(&toff[bin], 1u) : 0xffffffffu;
+      ent[i] = en;
     }
     __syncthreads();
-    // exclusive scan of toff[0, nbins): thread t owns bins [t·per_thr, (t+1)·per_thr)
+    // Warp w owns bins [w·wchunk, (w+1)·wchunk), lane l every 32nd of them (conflict-free).  First the
+    // runs are reserved at the global cursors — 16 atomics in flight per thread — then toff becomes the
+    // exclusive scan of the counts.
     {
-      const uint32_t b0 = tid * per_thr, b1 = min(B.nbins, b0 + per_thr);
-      uint32_t loc = 0;
-      for (uint32_t b = b0; b < b1; ++b) loc += toff[b];
-      uint32_t tot;
       const int lane = tid & 31, warp = tid >> 5;
-      uint32_t incl = loc;
+      const uint32_t w0 = warp * wchunk;
+      uint32_t wsum = 0;
+      for (uint32_t i0 = 0; i0 < wchunk; i0 += 32 * 16) {
+        uint32_t x[16], r[16];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t b = w0 + i0 + 32 * j + lane;
+          x[j] = (i0 + 32 * j < wchunk && b < B.nbins) ? toff[b] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + w0 + i0 + 32 * j + lane, x[j]) : 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (x[j]) base[w0 + i0 + 32 * j + lane] = r[j];
+          wsum += x[j];
+        }
       }
-      if (lane == 31) s_w[warp] = incl;
+      wsum = warp_sum(wsum);
+      if (lane == 0) s_w[warp] = wsum;
       __syncthreads();
-      uint32_t run = incl - loc;
-      tot = 0;
+      uint32_t carry = 0, tot = 0;
       for (int w = 0; w < kBinThreads / 32; ++w) {
-        run += w < warp ? s_w[w] : 0u;
+        carry += w < warp ? s_w[w] : 0u;
         tot += s_w[w];
       }
-      for (uint32_t b = b0; b < b1; ++b) {
-        const uint32_t x = toff[b];
-        toff[b] = run;
-        run += x;
+      for (uint32_t i = 0; i < wchunk; i += 32) {
+        const uint32_t b = w0 + i + lane;
+        const uint32_t x = b < B.nbins ? toff[b] : 0u;
+        uint32_t incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (b < B.nbins) {
+          const uint32_t ex = carry + incl - x;
+          toff[b] = ex;
+          if (x) base[b] -= ex;   // base[b] + p is the slot of staging position p
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
       if (tid == 0) toff[B.nbins] = tot;
     }
@@ -242,15 +233,23 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const __grid_consta
     __syncthreads();
     const uint32_t total = toff[B.nbins];
     for (uint32_t p = tid; p < total; p += kBinThreads) {
-      const uint32_t b = sbin[p];
-      entries[base[b] + (p - toff[b])] = stage[p];
+      entries[base[sbin[p]] + p] = stage[p];
     }
-    __syncthreads();
-    for (uint32_t b = tid; b < B.nbins; b += kBinThreads) base[b] += toff[b + 1] - toff[b];
     __syncthreads();
     for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
     __syncthreads();
   }
+}
+
+// Shared-memory test-and-set pieces of k_bin_apply, on 32-bit shared addresses.  A load may see a stale
+// 0 (the bit set by another thread meanwhile): that only costs a redundant RED, never a lost bit.
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void reds_or(uint32_t a, uint32_t bit) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit));
 }
 
 // Column of array a for LP (P:235 RA: CL_bs window of LP; P:239 VA: H_j(LP)).
@@ -262,13 +261,14 @@ __device__ __forceinline__ uint32_t lp_col(const Geo& G, uint64_t dbl, uint32_t 
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the
 // group (word i = word w of column i of CS cs, columns of all arrays in S:116 order), which is then
 // OR-ed into the cube.  The CTA owns those words for the whole launch.  <3, 1>: paper shape unrolled.
-template <int NRA, int NVA>
+template <int NRA, int NVA, bool ATOMS_ONLY>
 __global__ void __launch_bounds__(kApplyThreads) k_bin_apply(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
-                                                             const uint32_t* __restrict__ offs,
+                                                             const uint32_t* __restrict__ start,
                                                              const uint32_t* __restrict__ entries,
                                                              uint32_t* __restrict__ cube) {
   extern __shared__ uint32_t sub[];
+  const uint32_t sbase = smem_addr(sub);
   const uint32_t wg = blockIdx.x, cs = wg >> G.wpc_log2, w = wg & (G.wpc - 1u);
   for (uint32_t i = threadIdx.x; i < B.ncols; i += kApplyThreads) sub[i] = 0;
   uint32_t cbase[CBAA_MAX_ARRAYS];
@@ -276,38 +276,70 @@ __global__ void __launch_bounds__(kApplyThreads) k_bin_apply(const __grid_consta
 #pragma unroll
   for (uint32_t a = 0; a < CBAA_MAX_ARRAYS; ++a) cbase[a] = a < narr ? G.arr_off[a] >> G.wpc_log2 : 0u;
   __syncthreads();
+  // the word group's bins are adjacent in the entry array: one range [P0, P1), bin k of the group gives
+  // row bits k << s; loads of the next batch are issued before the current batch is applied
   const uint32_t kb = 1u << (5 - B.s), b0 = (cs << B.bpc_log2) + w * kb, smask = (1u << B.s) - 1u;
-  for (uint32_t k = 0; k < kb; ++k) {
-    const uint32_t p0 = offs[(uint64_t)(b0 + k) * B.nblk], p1 = offs[(uint64_t)(b0 + k + 1) * B.nblk];
-    const uint32_t hi = k << B.s;
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += 4 * kApplyThreads) {
-      uint32_t e[4];
+  const uint32_t P0 = start[b0], P1 = start[b0 + kb], B1 = kb > 1 ? start[b0 + 1] : P1;
+  // paper shape: per-array shift, mask and shared base address held in registers
+  uint32_t shv[NRA > 0 ? NRA : 1], mk[NRA > 0 ? NRA + NVA : 1], ab[NRA > 0 ? NRA + NVA : 1];
+  if constexpr (NRA > 0) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t q = p + u * kApplyThreads;
-        e[u] = q < p1 ? __ldcs(entries + q) : 0xffffffffu;
+    for (int a = 0; a < NRA + NVA; ++a) {
+      if (a < NRA) shv[a] = G.sh[a];
+      mk[a] = G.colmask[a];
+      ab[a] = sbase + 4u * cbase[a];
+    }
+  }
+  auto apply_one = [&](uint32_t e, uint32_t q) {
+    uint32_t hi = 0;
+    if (kb == 2) hi = q >= B1 ? 1u << B.s : 0u;
+    else if (kb > 2)
+      for (uint32_t k = 1; k < kb; ++k) hi += q >= start[b0 + k] ? 1u << B.s : 0u;
+    const uint32_t lp = e >> B.s, bit = 1u << (hi | (e & smask));
+    const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+    if constexpr (NRA > 0) {
+      uint32_t adr[NRA + NVA];
+#pragma unroll
+      for (int a = 0; a < NRA + NVA; ++a) {
+        const uint32_t col = a < NRA ? (uint32_t)(dbl >> shv[a < NRA ? a : 0]) & mk[a]
+                                     : mix32(lp ^ G.va_seeds[a - NRA]) & mk[a];
+        adr[a] = ab[a] + 4u * col;
       }
+      if constexpr (ATOMS_ONLY) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (p + u * kApplyThreads >= p1) continue;
-        const uint32_t lp = e[u] >> B.s, bit = 1u << (hi | (e[u] & smask));
-        const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
-        if constexpr (NRA > 0) {
+        for (int a = 0; a < NRA + NVA; ++a) reds_or(adr[a], bit);
+      } else {
+        uint32_t v[NRA + NVA];
 #pragma unroll
-          for (int a = 0; a < NRA + NVA; ++a) {
-            const uint32_t col = a < NRA ? (uint32_t)(dbl >> G.sh[a]) & G.colmask[a]
-                                         : mix32(lp ^ G.va_seeds[a - NRA]) & G.colmask[a];
-            uint32_t* x = sub + cbase[a] + col;
-            if (!(*x & bit)) atomicOr(x, bit);
-          }
-        } else {
-          for (uint32_t a = 0; a < narr; ++a) {
-            uint32_t* x = sub + (G.arr_off[a] >> G.wpc_log2) + lp_col(G, dbl, lp, a);
-            if (!(*x & bit)) atomicOr(x, bit);
-          }
-        }
+        for (int a = 0; a < NRA + NVA; ++a) v[a] = lds(adr[a]);
+#pragma unroll
+        for (int a = 0; a < NRA + NVA; ++a)
+          if (!(v[a] & bit)) reds_or(adr[a], bit);
+      }
+    } else {
+      for (uint32_t a = 0; a < narr; ++a) {
+        const uint32_t adr = sbase + 4u * ((G.arr_off[a] >> G.wpc_log2) + lp_col(G, dbl, lp, a));
+        if (ATOMS_ONLY || !(lds(adr) & bit)) reds_or(adr, bit);
       }
     }
+  };
+  constexpr uint32_t kStep = kApplyUnroll * kApplyThreads;
+  uint32_t e[kApplyUnroll];
+  uint32_t p = P0 + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kApplyThreads < P1 ? __ldcs(entries + p + u * kApplyThreads) : 0u;
+  while (p < P1) {
+    const uint32_t pn = p + kStep;
+    uint32_t en[kApplyUnroll];
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      en[u] = pn + u * kApplyThreads < P1 ? __ldcs(entries + pn + u * kApplyThreads) : 0u;
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      if (p + u * kApplyThreads < P1) apply_one(e[u], p + u * kApplyThreads);
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
+    p = pn;
   }
   __syncthreads();
   uint32_t* cw = cube + (uint64_t)cs * G.cs_words + w;

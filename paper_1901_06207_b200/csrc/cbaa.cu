@@ -77,10 +77,16 @@ struct cbaa_handle {
   int binnable = 0;          // geometry fits the binned kernels' shared-memory tables
   uint64_t bin_min = 0;      // fewer pairs per call than this take the direct kernel
   uint64_t bin_chunk = 1ull << 28;   // pairs per count/scatter/apply round (CBAA_BIN_CHUNK, tests)
+  int apply_atoms = 0;       // CBAA_APPLY_ATOMS=1: k_bin_apply ORs every bit without the test (A/B)
   uint32_t* bin_ent = nullptr;
   uint64_t bin_cap = 0;
-  uint32_t* bin_offs = nullptr;   // [nbins · nblk + 1]
-  uint32_t* bin_part = nullptr;
+  uint32_t* bin_tab = nullptr;    // counts | start | cursor
+  // per-kernel update timing (cbaa_set_phase_timing)
+  int timing = 0;
+  std::vector<cudaEvent_t> tev;   // pairs: tev[2k], tev[2k+1]
+  std::vector<int> tphase;        // phase of pair k
+  size_t tused = 0;
+  uint64_t tcalls = 0;
   std::string err;
 };
 
@@ -342,7 +348,7 @@ void dispatch_update(const cbaa_handle* h, F&& f) {
   using T = std::integral_constant<int, CBAA_UPDATE_TEST_SET>;
   using R = std::integral_constant<int, CBAA_UPDATE_RED>;
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-  const bool test = h->cfg.update_mode == CBAA_UPDATE_TEST_SET;
+  const bool test = h->cfg.update_mode != CBAA_UPDATE_RED;   // BINNED falls back to test-and-set
   auto go = [&](auto nra, auto nva) {
     if (test) {
       if (prefix) f(nra, nva, T{}, std::true_type{});
@@ -399,12 +405,30 @@ int launch_update_aos(cbaa_handle* h, const uint32_t* pairs, uint64_t n, uint32_
   return launch_check(h, "k_update_aos");
 }
 
-// Binned update (binned.cuh): count → scan → scatter → apply, in chunks of at most 2^28 pairs.
+// Phase timing: t_begin records the start event of the next kernel (returns its slot, or -1 when off);
+// t_end records its end.
+int t_begin(cbaa_handle* h, int phase, cudaStream_t s) {
+  if (!h->timing) return -1;
+  if (h->tused == h->tphase.size()) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return -1;
+    h->tev.push_back(a);
+    h->tev.push_back(b);
+    h->tphase.push_back(0);
+  }
+  const size_t k = h->tused++;
+  h->tphase[k] = phase;
+  cudaEventRecord(h->tev[2 * k], s);
+  return (int)k;
+}
+void t_end(cbaa_handle* h, int k, cudaStream_t s) {
+  if (k >= 0) cudaEventRecord(h->tev[2 * k + 1], s);
+}
+
+// Binned update (binned.cuh): count → starts → scatter → apply, in chunks of at most 2^28 pairs.
 int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t kChunk = h->bin_chunk;
   const BinGeo& B = h->B;
-  const uint64_t m_cnt = (uint64_t)B.nbins * B.nblk;
-  const uint32_t n_part = (uint32_t)((m_cnt + kScanSeg - 1) / kScanSeg);
   const uint64_t want = std::min(n, kChunk);
   if (h->bin_cap < want) {
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
@@ -413,10 +437,13 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     CK(h, cudaMalloc(&h->bin_ent, want * 4));
     h->bin_cap = want;
   }
-  if (!h->bin_offs) {
-    CK(h, cudaMalloc(&h->bin_offs, (m_cnt + 1) * 4));
-    CK(h, cudaMalloc(&h->bin_part, (uint64_t)n_part * 4));
+  if (!h->bin_tab) {   // counts [nbins] | start [nbins + 1] | cursor [nbins]
+    CK(h, cudaMalloc(&h->bin_tab, (3ull * B.nbins + 1) * 4));
+    CK(h, cudaMemsetAsync(h->bin_tab, 0, (uint64_t)B.nbins * 4, s));
   }
+  uint32_t* counts = h->bin_tab;
+  uint32_t* start = counts + B.nbins;
+  uint32_t* cursor = start + B.nbins + 1;
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
   const size_t sm_cnt = (size_t)B.nbins * 4;
   const size_t sm_sc = (size_t)(2 * B.nbins + 1) * 4 + (size_t)kBinTile * 6;
@@ -428,33 +455,46 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     const uint32_t* b = dst + off;
     const uint64_t per = (((m + B.nblk - 1) / B.nblk) + 3) & ~3ull;
     const int vec = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
-    if (prefix) k_bin_count<true><<<B.nblk, kBinThreads, sm_cnt, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->skipped);
-    else k_bin_count<false><<<B.nblk, kBinThreads, sm_cnt, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, nullptr);
+    const uint32_t nc = 2 * (uint32_t)h->sms;   // count grid: any chunking works (global totals)
+    const uint64_t per_c = (((m + nc - 1) / nc) + 3) & ~3ull;
+    int tk = t_begin(h, 0, s);
+    if (prefix) k_bin_count<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, h->skipped);
+    else k_bin_count<false><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, nullptr);
+    t_end(h, tk, s);
     int rc = launch_check(h, "k_bin_count");
     if (rc) return rc;
-    k_bin_scan_reduce<<<n_part, kBinThreads, 0, s>>>(h->bin_offs, m_cnt, h->bin_part);
-    if ((rc = launch_check(h, "k_bin_scan_reduce"))) return rc;
-    k_bin_scan_down<<<n_part, kBinThreads, 0, s>>>(h->bin_offs, m_cnt, h->bin_part);
-    if ((rc = launch_check(h, "k_bin_scan_down"))) return rc;
-    if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->bin_ent);
-    else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, h->bin_offs, h->bin_ent);
+    tk = t_begin(h, 1, s);
+    k_bin_starts<<<1, kStartThreads, 0, s>>>(B.nbins, counts, start, cursor);
+    t_end(h, tk, s);
+    if ((rc = launch_check(h, "k_bin_starts"))) return rc;
+    tk = t_begin(h, 2, s);
+    if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+    else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+    t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_scatter"))) return rc;
-    if (h->G.num_ra == 3 && h->G.num_va == 1)
-      k_bin_apply<3, 1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, h->bin_offs, h->bin_ent, h->cube);
-    else
-      k_bin_apply<0, 0><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, h->bin_offs, h->bin_ent, h->cube);
+    tk = t_begin(h, 3, s);
+    if (h->G.num_ra == 3 && h->G.num_va == 1) {
+      if (h->apply_atoms) k_bin_apply<3, 1, true><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+      else k_bin_apply<3, 1, false><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+    } else {
+      k_bin_apply<0, 0, false><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+    }
+    t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
   }
   return CBAA_OK;
 }
 
 int update_all_passes(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
+  ++h->tcalls;
   if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min)
     return update_binned(h, src, dst, n, s);
   const uint64_t W = h->cube_words;
   for (uint32_t p = 0; p < h->passes; ++p) {
     uint64_t lo = W * p / h->passes, hi = W * (p + 1) / h->passes;
+    const int tk = t_begin(h, 0, s);
     int rc = launch_update(h, src, dst, n, (uint32_t)lo, (uint32_t)(hi - lo), p == 0, s);
+    t_end(h, tk, s);
     if (rc) return rc;
   }
   return CBAA_OK;
@@ -491,6 +531,7 @@ int cbaa_config_default(cbaa_config* out) {
   out->theta_formula = CBAA_THETA_PAPER;
   out->direction = CBAA_DIR_NORMALIZED;
   out->tuple_cap = 1ull << 24;
+  out->update_mode = CBAA_UPDATE_BINNED;   // large windows binned, small ones test-and-set
   return CBAA_OK;
 }
 
@@ -583,11 +624,13 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     B.nbins = h->G.n_cs << B.bpc_log2;
     B.nblk = (uint32_t)h->sms * 2;
     B.ncols = h->G.cs_words / h->G.wpc;
-    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;
+    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;   // scatter tables ≤ 224 KiB, word group ≤ 112 KiB
     const char* bm = std::getenv("CBAA_BIN_MIN");
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
                  : bm                 ? std::strtoull(bm, nullptr, 10)
                                       : std::max<uint64_t>(1u << 20, h->cube_words / 4);
+    const char* aa = std::getenv("CBAA_APPLY_ATOMS");
+    h->apply_atoms = aa && aa[0] == '1';
     const char* bc = std::getenv("CBAA_BIN_CHUNK");
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
@@ -597,8 +640,9 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_apply<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
-      cudaFuncSetAttribute(k_bin_apply<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<3, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<0, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
     }
   }
   int occ = 0;
@@ -618,8 +662,8 @@ void cbaa_destroy(cbaa_handle* h) {
   if (h->cube && !h->cube_external) cudaFree(h->cube);
   if (h->scratch) cudaFree(h->scratch);
   if (h->bin_ent) cudaFree(h->bin_ent);
-  if (h->bin_offs) cudaFree(h->bin_offs);
-  if (h->bin_part) cudaFree(h->bin_part);
+  if (h->bin_tab) cudaFree(h->bin_tab);
+  for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
   if (h->prefix_bits) cudaFree(h->prefix_bits);
   if (h->D.cand) cudaFree(h->D.cand);
   if (h->h_rec) cudaFreeHost(h->h_rec);
@@ -1177,5 +1221,29 @@ int cbaa_ipc_close(cbaa_handle* h, void* dev_ptr) {
 uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0; }
 
 uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }
+
+int cbaa_set_phase_timing(cbaa_handle* h, int enable) {
+  if (!h) return CBAA_E_ARG;
+  h->timing = enable ? 1 : 0;
+  h->tused = 0;
+  h->tcalls = 0;
+  return CBAA_OK;
+}
+
+int cbaa_update_phase_ms(cbaa_handle* h, double* ms, int cap, uint64_t* calls) {
+  if (!h || !ms || cap < 4) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  for (int i = 0; i < 4; ++i) ms[i] = 0;
+  for (size_t k = 0; k < h->tused; ++k) {
+    CK(h, cudaEventSynchronize(h->tev[2 * k + 1]));
+    float t = 0;
+    CK(h, cudaEventElapsedTime(&t, h->tev[2 * k], h->tev[2 * k + 1]));
+    ms[h->tphase[k]] += t;
+  }
+  if (calls) *calls = h->tcalls;
+  h->tused = 0;
+  h->tcalls = 0;
+  return CBAA_OK;
+}
 
 }  // extern "C"

@@ -1,6 +1,7 @@
 """Direct (test-and-set) vs binned update on one B200: ms per update for C2 and other shapes —
     python tools/binned_perf.py > gpurun_out/binned_perf.jsonl"""
 import json
+import os
 import sys
 
 import numpy as np
@@ -33,13 +34,15 @@ def main():
         s = torch.from_numpy(w.src.view(np.int32)).cuda()
         d = torch.from_numpy(w.dst.view(np.int32)).cuda()
         ref = None
-        for mode in (0, 2):
+        for mode, staged, atoms in ((0, "1", "0"), (2, "1", "0")):
+            os.environ["CBAA_APPLY_ATOMS"] = atoms
             cb = Cbaa(config_from_dict(dict(p, update_mode=mode)), 0)
             med, best = t_update(cb, s, d)
             cube = cb.cube().clone()
             same = None if ref is None else bool(torch.equal(cube, ref))
             ref = cube if ref is None else ref
-            print(json.dumps({"case": name, "n": int(s.numel()), "mode": mode, "ms_median": round(med, 4),
+            print(json.dumps({"case": name, "n": int(s.numel()), "mode": mode, "staged": staged, "apply_atoms": atoms,
+                              "ms_median": round(med, 4),
                               "ms_best": round(best, 4), "gpairs_s": round(s.numel() / med / 1e6, 2),
                               "cube_equal_to_mode0": same}), flush=True)
             del cb

@@ -1,6 +1,6 @@
 """Small windows through every kernel, for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
     compute-sanitizer --tool memcheck python tools/sanitize.py
-Exercises update (both modes, aligned / misaligned / prefix), reset, merge, merge_slice, zero counts,
+Exercises update (all three modes incl. the binned kernels, aligned / misaligned / prefix), reset, merge, merge_slice, zero counts,
 detect (join and Cartesian paths), SketchFile round trip and debug_map; checks the cube against the oracle."""
 import os
 import sys
@@ -22,9 +22,9 @@ def main():
     w = W.generate(W.WindowSpec(n=60_000, n_hosts=3000, n_flows=20000, scanners=(1500, 2500), victims=(1800,)), 3)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
     ok = True
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         for extra in ({}, {"update_passes": 3}, {"direction": 1, "prefixes": w.prefixes}):
-            q = dict(p, update_mode=mode, **extra)
+            q = dict(p, update_mode=mode, bin_min_pairs=1, **extra)
             cb = Cbaa(config_from_dict(q), 0)
             cb.reset()
             s, d = (w.raw_src, w.raw_dst) if extra.get("direction") else (w.src, w.dst)
