@@ -48,6 +48,13 @@ __device__ __forceinline__ bool pair_bin(const Geo& G, const BinGeo& B, uint32_t
   return true;
 }
 
+__device__ __forceinline__ uint32_t vsum(uint4 v) { return v.x + v.y + v.z + v.w; }
+// Opaque to the optimizer: keeps a loop-invariant in a register instead of re-reading the parameter bank.
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+
 // Loads the 4 pairs starting at k of a CTA chunk ending at c1 (vector load when the group is whole and
 // both arrays are 16-B aligned at the chunk starts).
 __device__ __forceinline__ void load_quad(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
@@ -174,12 +181,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const __grid_con
     }
     __syncthreads();
     // Warp w owns bins [w·wchunk, (w+1)·wchunk), lane l every 32nd of them (conflict-free).  First the
-    // runs are reserved at the global cursors — 16 atomics in flight per thread — then toff becomes the
-    // exclusive scan of the counts.
+    // runs are reserved at the global cursors (a warp's 32 atomics hit one line of the cursors; 16 in
+    // flight per thread).  Then each bin gets its run in the staging array: the staging order only has
+    // to keep a bin's entries together, so it is thread-major — thread t's bins follow each other — and
+    // one scan of the per-thread totals places every run.
     {
       const int lane = tid & 31, warp = tid >> 5;
       const uint32_t w0 = warp * wchunk;
-      uint32_t wsum = 0;
+      uint32_t loc = 0;
       for (uint32_t i0 = 0; i0 < wchunk; i0 += 32 * 16) {
         uint32_t x[16], r[16];
 #pragma unroll
@@ -192,32 +201,34 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const __grid_con
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (x[j]) base[w0 + i0 + 32 * j + lane] = r[j];
-          wsum += x[j];
+          loc += x[j];
         }
       }
-      wsum = warp_sum(wsum);
-      if (lane == 0) s_w[warp] = wsum;
+      uint32_t incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_w[warp] = incl;
       __syncthreads();
-      uint32_t carry = 0, tot = 0;
+      uint32_t run = incl - loc, tot = 0;
+#pragma unroll
       for (int w = 0; w < kBinThreads / 32; ++w) {
-        carry += w < warp ? s_w[w] : 0u;
+        run += w < warp ? s_w[w] : 0u;
         tot += s_w[w];
       }
-      for (uint32_t i = 0; i < wchunk; i += 32) {
-        const uint32_t b = w0 + i + lane;
-        const uint32_t x = b < B.nbins ? toff[b] : 0u;
-        uint32_t incl = x;
+      for (uint32_t i0 = 0; i0 < wchunk; i0 += 32 * 16) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t b = w0 + i0 + 32 * j + lane;
+          if (i0 + 32 * j < wchunk && b < B.nbins) {
+            const uint32_t x = toff[b];
+            toff[b] = run;
+            if (x) base[b] -= run;   // base[b] + p is the slot of staging position p
+            run += x;
+          }
         }
-        if (b < B.nbins) {
-          const uint32_t ex = carry + incl - x;
-          toff[b] = ex;
-          if (x) base[b] -= ex;   // base[b] + p is the slot of staging position p
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
       if (tid == 0) toff[B.nbins] = tot;
     }
@@ -261,14 +272,15 @@ __device__ __forceinline__ uint32_t lp_col(const Geo& G, uint64_t dbl, uint32_t 
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the
 // group (word i = word w of column i of CS cs, columns of all arrays in S:116 order), which is then
 // OR-ed into the cube.  The CTA owns those words for the whole launch.  <3, 1>: paper shape unrolled.
-template <int NRA, int NVA, bool ATOMS_ONLY>
-__global__ void __launch_bounds__(kApplyThreads) k_bin_apply(const __grid_constant__ Geo G,
+template <int NRA, int NVA, int S>
+__global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ start,
                                                              const uint32_t* __restrict__ entries,
                                                              uint32_t* __restrict__ cube) {
+  // S: entry row bits known at compile time (4 = the paper's r = 4, hence also L = 28), −1: run time
   extern __shared__ uint32_t sub[];
-  const uint32_t sbase = smem_addr(sub);
+  const uint32_t sbase = pin(smem_addr(sub));
   const uint32_t wg = blockIdx.x, cs = wg >> G.wpc_log2, w = wg & (G.wpc - 1u);
   for (uint32_t i = threadIdx.x; i < B.ncols; i += kApplyThreads) sub[i] = 0;
   uint32_t cbase[CBAA_MAX_ARRAYS];
@@ -278,48 +290,45 @@ __global__ void __launch_bounds__(kApplyThreads) k_bin_apply(const __grid_consta
   __syncthreads();
   // the word group's bins are adjacent in the entry array: one range [P0, P1), bin k of the group gives
   // row bits k << s; loads of the next batch are issued before the current batch is applied
-  const uint32_t kb = 1u << (5 - B.s), b0 = (cs << B.bpc_log2) + w * kb, smask = (1u << B.s) - 1u;
-  const uint32_t P0 = start[b0], P1 = start[b0 + kb], B1 = kb > 1 ? start[b0 + 1] : P1;
-  // paper shape: per-array shift, mask and shared base address held in registers
+  const uint32_t es = S >= 0 ? (uint32_t)S : B.s;
+  const uint32_t L = (S >= 0 && S < 5) ? 32u - (uint32_t)S : G.L;   // s < 5 ⇔ r = s
+  const uint32_t kb = 1u << (5 - es), b0 = (cs << B.bpc_log2) + w * kb, smask = (1u << es) - 1u;
+  const uint32_t P0 = start[b0], P1 = start[b0 + kb], B1 = pin(kb > 1 ? start[b0 + 1] : P1);
+  // paper shape: per-array shift, mask and shared base address pinned in registers
   uint32_t shv[NRA > 0 ? NRA : 1], mk[NRA > 0 ? NRA + NVA : 1], ab[NRA > 0 ? NRA + NVA : 1];
+  uint32_t vseed = 0;
   if constexpr (NRA > 0) {
 #pragma unroll
     for (int a = 0; a < NRA + NVA; ++a) {
-      if (a < NRA) shv[a] = G.sh[a];
-      mk[a] = G.colmask[a];
-      ab[a] = sbase + 4u * cbase[a];
+      if (a < NRA) shv[a] = pin(G.sh[a]);
+      mk[a] = pin(G.colmask[a]);
+      ab[a] = pin(sbase + 4u * cbase[a]);
     }
+    if constexpr (NVA == 1) vseed = pin(G.va_seeds[0]);
   }
   auto apply_one = [&](uint32_t e, uint32_t q) {
     uint32_t hi = 0;
-    if (kb == 2) hi = q >= B1 ? 1u << B.s : 0u;
+    if (kb == 2) hi = q >= B1 ? 1u << es : 0u;
     else if (kb > 2)
-      for (uint32_t k = 1; k < kb; ++k) hi += q >= start[b0 + k] ? 1u << B.s : 0u;
-    const uint32_t lp = e >> B.s, bit = 1u << (hi | (e & smask));
-    const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+      for (uint32_t k = 1; k < kb; ++k) hi += q >= start[b0 + k] ? 1u << es : 0u;
+    const uint32_t lp = e >> es, bit = 1u << (hi | (e & smask));
+    const uint64_t dbl = ((uint64_t)lp << L) | lp;
     if constexpr (NRA > 0) {
-      uint32_t adr[NRA + NVA];
+      uint32_t adr[NRA + NVA], v[NRA + NVA];
 #pragma unroll
       for (int a = 0; a < NRA + NVA; ++a) {
         const uint32_t col = a < NRA ? (uint32_t)(dbl >> shv[a < NRA ? a : 0]) & mk[a]
-                                     : mix32(lp ^ G.va_seeds[a - NRA]) & mk[a];
+                                     : mix32(lp ^ (NVA == 1 ? vseed : G.va_seeds[a - NRA])) & mk[a];
         adr[a] = ab[a] + 4u * col;
+        v[a] = lds(adr[a]);
       }
-      if constexpr (ATOMS_ONLY) {
 #pragma unroll
-        for (int a = 0; a < NRA + NVA; ++a) reds_or(adr[a], bit);
-      } else {
-        uint32_t v[NRA + NVA];
-#pragma unroll
-        for (int a = 0; a < NRA + NVA; ++a) v[a] = lds(adr[a]);
-#pragma unroll
-        for (int a = 0; a < NRA + NVA; ++a)
-          if (!(v[a] & bit)) reds_or(adr[a], bit);
-      }
+      for (int a = 0; a < NRA + NVA; ++a)
+        if (!(v[a] & bit)) reds_or(adr[a], bit);
     } else {
       for (uint32_t a = 0; a < narr; ++a) {
         const uint32_t adr = sbase + 4u * ((G.arr_off[a] >> G.wpc_log2) + lp_col(G, dbl, lp, a));
-        if (ATOMS_ONLY || !(lds(adr) & bit)) reds_or(adr, bit);
+        if (!(lds(adr) & bit)) reds_or(adr, bit);
       }
     }
   };

@@ -77,7 +77,6 @@ struct cbaa_handle {
   int binnable = 0;          // geometry fits the binned kernels' shared-memory tables
   uint64_t bin_min = 0;      // fewer pairs per call than this take the direct kernel
   uint64_t bin_chunk = 1ull << 28;   // pairs per count/scatter/apply round (CBAA_BIN_CHUNK, tests)
-  int apply_atoms = 0;       // CBAA_APPLY_ATOMS=1: k_bin_apply ORs every bit without the test (A/B)
   uint32_t* bin_ent = nullptr;
   uint64_t bin_cap = 0;
   uint32_t* bin_tab = nullptr;    // counts | start | cursor
@@ -473,12 +472,12 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_scatter"))) return rc;
     tk = t_begin(h, 3, s);
-    if (h->G.num_ra == 3 && h->G.num_va == 1) {
-      if (h->apply_atoms) k_bin_apply<3, 1, true><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
-      else k_bin_apply<3, 1, false><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
-    } else {
-      k_bin_apply<0, 0, false><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
-    }
+    if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
+      k_bin_apply<3, 1, 4><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+    else if (h->G.num_ra == 3 && h->G.num_va == 1)
+      k_bin_apply<3, 1, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+    else
+      k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
   }
@@ -624,25 +623,25 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     B.nbins = h->G.n_cs << B.bpc_log2;
     B.nblk = (uint32_t)h->sms * 2;
     B.ncols = h->G.cs_words / h->G.wpc;
-    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;   // scatter tables ≤ 224 KiB, word group ≤ 112 KiB
+    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;   // scatter tables ≤ 176 KiB, word group ≤ 112 KiB
     const char* bm = std::getenv("CBAA_BIN_MIN");
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
                  : bm                 ? std::strtoull(bm, nullptr, 10)
                                       : std::max<uint64_t>(1u << 20, h->cube_words / 4);
-    const char* aa = std::getenv("CBAA_APPLY_ATOMS");
-    h->apply_atoms = aa && aa[0] == '1';
     const char* bc = std::getenv("CBAA_BIN_CHUNK");
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
     if (h->binnable) {
-      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)(2 * B.nbins + 1) * 4 + kBinTile * 6, sm_ap = (int)B.ncols * 4;
+      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((2 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
       cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_apply<3, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
-      cudaFuncSetAttribute(k_bin_apply<3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
-      cudaFuncSetAttribute(k_bin_apply<0, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_bin_apply<3, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
     }
   }
   int occ = 0;

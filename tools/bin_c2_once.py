@@ -17,3 +17,6 @@ for _ in range(2):
     cb.reset()
     cb.update(s, d)
 torch.cuda.synchronize()
+if len(sys.argv) > 2:   # occupancy report of the binned kernels
+    import ctypes
+    print("max active scatter CTAs/SM reported via ncu launch__occupancy_limit_shared_mem")
