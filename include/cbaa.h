@@ -97,7 +97,8 @@ typedef struct {
                                        /* windows): window-end kernels use no shared memory so they fit   */
                                        /* next to the update's CTAs; 0: fastest standalone detect (TMA)   */
   uint32_t bin_min_pairs;              /* CBAA_UPDATE_BINNED: calls with fewer pairs take the direct      */
-                                       /* kernel (0 = auto: max(2^20, cube words / 4))                    */
+                                       /* kernel (0 = auto: max(2^20, cube words / 4), and cubes up to    */
+                                       /* 0.6 of L2 always direct)                                         */
   uint32_t reserved[2];
 } cbaa_config;
 

@@ -49,6 +49,12 @@ __device__ __forceinline__ bool pair_bin(const Geo& G, const BinGeo& B, uint32_t
 }
 
 __device__ __forceinline__ uint32_t vsum(uint4 v) { return v.x + v.y + v.z + v.w; }
+// Shared-memory fetch-and-increment on a 32-bit shared address.
+__device__ __forceinline__ uint32_t atoms_inc(uint32_t a) {
+  uint32_t v;
+  asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(a));
+  return v;
+}
 // Opaque to the optimizer: keeps a loop-invariant in a register instead of re-reading the parameter bank.
 __device__ __forceinline__ uint32_t pin(uint32_t x) {
   asm volatile("" : "+r"(x));
@@ -163,21 +169,43 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const __grid_con
   for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t wchunk = (B.nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
+  const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), pgm = pin(G.g - 1u);
+  const uint32_t prm = pin(G.rmask), pr = pin(G.r), pbl = pin(B.bpc_log2), pes = pin(B.s);
+  const uint32_t psm = pin((1u << B.s) - 1u), toff_sa = pin(smem_addr(toff));
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
     // all kBinPPT pairs of the thread are loaded before any is hashed (one DRAM latency per tile), then
     // each pair's registers are reused for its key (bin, rank in the tile) and entry
     uint32_t key[kBinPPT], ent[kBinPPT];
-    bool in[kBinPPT];
+    if (!PREFIX && vec && t0 + kBinTile <= c1) {
+      // whole tile, normalised input: no per-pair checks; parameters pinned in registers
 #pragma unroll
-    for (int q = 0; q < kBinPPT / 4; ++q)
-      load_quad(src, dst, t0 + 4ull * ((uint64_t)q * kBinThreads + tid), c1, vec, key + 4 * q, ent + 4 * q, in + 4 * q);
+      for (int q = 0; q < kBinPPT / 4; ++q) {
+        const uint64_t k = t0 + 4ull * ((uint64_t)q * kBinThreads + tid);
+        const uint4 a = ld_stream4(src + k), b = ld_stream4(dst + k);
+        key[4 * q] = a.x, key[4 * q + 1] = a.y, key[4 * q + 2] = a.z, key[4 * q + 3] = a.w;
+        ent[4 * q] = b.x, ent[4 * q + 1] = b.y, ent[4 * q + 2] = b.z, ent[4 * q + 3] = b.w;
+      }
 #pragma unroll
-    for (int i = 0; i < kBinPPT; ++i) {
-      uint32_t bin = 0, en = 0;
-      const bool ok = in[i] && pair_bin<PREFIX>(G, B, key[i], ent[i], bin, en);
-      key[i] = ok ? (bin << kBinRankBits) | atomicAdd(&toff[bin], 1u) : 0xffffffffu;
-      ent[i] = en;
+      for (int i = 0; i < kBinPPT; ++i) {
+        const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;           // P:175, Q2
+        const uint32_t row = mix32(mo ^ pbv) & pgm;
+        const uint32_t bin = ((mi & prm) << pbl) | (row >> pes);              // (cs, row >> s)
+        ent[i] = ((mi >> pr) << pes) | (row & psm);                           // LP, low row bits
+        key[i] = (bin << kBinRankBits) | atoms_inc(toff_sa + 4u * bin);
+      }
+    } else {
+      bool in[kBinPPT];
+#pragma unroll
+      for (int q = 0; q < kBinPPT / 4; ++q)
+        load_quad(src, dst, t0 + 4ull * ((uint64_t)q * kBinThreads + tid), c1, vec, key + 4 * q, ent + 4 * q, in + 4 * q);
+#pragma unroll
+      for (int i = 0; i < kBinPPT; ++i) {
+        uint32_t bin = 0, en = 0;
+        const bool ok = in[i] && pair_bin<PREFIX>(G, B, key[i], ent[i], bin, en);
+        key[i] = ok ? (bin << kBinRankBits) | atomicAdd(&toff[bin], 1u) : 0xffffffffu;
+        ent[i] = en;
+      }
     }
     __syncthreads();
     // Warp w owns bins [w·wchunk, (w+1)·wchunk), lane l every 32nd of them (conflict-free).  First the
@@ -343,9 +371,14 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
 #pragma unroll
     for (int u = 0; u < kApplyUnroll; ++u)
       en[u] = pn + u * kApplyThreads < P1 ? __ldcs(entries + pn + u * kApplyThreads) : 0u;
+    if (p + (kApplyUnroll - 1) * kApplyThreads < P1) {   // whole batch: no per-entry bound checks
 #pragma unroll
-    for (int u = 0; u < kApplyUnroll; ++u)
-      if (p + u * kApplyThreads < P1) apply_one(e[u], p + u * kApplyThreads);
+      for (int u = 0; u < kApplyUnroll; ++u) apply_one(e[u], p + u * kApplyThreads);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kApplyUnroll; ++u)
+        if (p + u * kApplyThreads < P1) apply_one(e[u], p + u * kApplyThreads);
+    }
 #pragma unroll
     for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
     p = pn;

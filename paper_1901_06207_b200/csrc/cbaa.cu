@@ -623,7 +623,12 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     B.nbins = h->G.n_cs << B.bpc_log2;
     B.nblk = (uint32_t)h->sms * 2;
     B.ncols = h->G.cs_words / h->G.wpc;
-    h->binnable = B.nbins <= 16384 && B.ncols <= 28672;   // scatter tables ≤ 176 KiB, word group ≤ 112 KiB
+    // scatter tables ≤ 48 KiB (≥ 2 pairs per bin in an 8192-pair tile), word group ≤ 112 KiB
+    h->binnable = B.nbins <= 4096 && B.ncols <= 28672;
+    // auto (bin_min_pairs = 0): cubes up to 0.6 of L2 stay on the direct kernel, whose random accesses then
+    // hit L2 (C5 sweep, profiles/r01_sweep_c5.jsonl: r = 2 and 8-64 MiB cubes are faster direct)
+    if (!cfg->bin_min_pairs && h->cube_bytes <= 0.6 * (double)(h->l2_bytes > 0 ? h->l2_bytes : (126 << 20)))
+      h->binnable = 0;
     const char* bm = std::getenv("CBAA_BIN_MIN");
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
                  : bm                 ? std::strtoull(bm, nullptr, 10)

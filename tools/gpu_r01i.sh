@@ -1,5 +1,8 @@
 set -x
-# functional N=2 run of the bench's multi-router path on a 1-GPU box (both ranks share GPU 0; the
-# timing is meaningless, the point is the ipc exchange + owned-range detect + gather + max-over-ranks)
-CBAA_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29561 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_n2_func.json 2> gpurun_out/bench_n2_func.err; echo rc=$?
-tail -c 1500 gpurun_out/bench_n2_func.json; tail -5 gpurun_out/bench_n2_func.err
+python __graft_entry__.py build > gpurun_out/build_r01i.log 2>&1; tail -1 gpurun_out/build_r01i.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_r01i.log 2>&1; tail -3 gpurun_out/pytest_r01i.log
+timeout 600 python tools/binned_perf.py > gpurun_out/binned_perf_i.jsonl 2> gpurun_out/binned_perf_i.err; head -2 gpurun_out/binned_perf_i.jsonl
+timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:"k_bin" --csv --log-file gpurun_out/launches_r01i.csv python tools/bin_c2_once.py > /dev/null 2>&1
+python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_r01i.json 2> gpurun_out/bench_r01i.err; python -c "import json;d=json.load(open('gpurun_out/bench_r01i.json'));print({k:d[k] for k in ('value','ms_per_step','ms_per_step_serial','update_ms','detect_ms')})"
+timeout 1500 python -m tests.sweep_c5 > gpurun_out/sweep_c5_i.jsonl 2> gpurun_out/sweep_c5_i.err; tail -2 gpurun_out/sweep_c5_i.err
+timeout 1500 python -m tests.full_c4 > gpurun_out/full_c4_i.jsonl 2> gpurun_out/full_c4_i.err; tail -2 gpurun_out/full_c4_i.jsonl
