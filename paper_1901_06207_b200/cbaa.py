@@ -14,6 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcbaa.so")
+LIB_PATH = os.environ.get("CBAA_LIB", LIB_PATH)   # A/B builds of the same sources (tools/)
 
 MAX_RA, MAX_VA, MAX_ARRAYS, MAX_PREFIXES = 8, 8, 16, 16
 

@@ -28,8 +28,18 @@ struct BinGeo {
   uint32_t ncols;      // Σc(i): words of one word group
 };
 
-constexpr int kBinThreads = 256;                   // k_bin_scatter: two CTAs per SM (128 regs × 512 = the RF);
-constexpr int kBinPPT = 32;                        // one 512-thread CTA with 16K-pair tiles measured 9 % slower
+#ifndef CBAA_BIN_THREADS
+#define CBAA_BIN_THREADS 256
+#endif
+#ifndef CBAA_BIN_PPT
+#define CBAA_BIN_PPT 32
+#endif
+#ifndef CBAA_BIN_MINB
+#define CBAA_BIN_MINB 2
+#endif
+constexpr int kBinMinBlocks = CBAA_BIN_MINB;       // k_bin_scatter CTAs per SM (grid = SMs × this)
+constexpr int kBinThreads = CBAA_BIN_THREADS;      // k_bin_scatter: two CTAs per SM (128 regs × 512 = the RF);
+constexpr int kBinPPT = CBAA_BIN_PPT;              // one 512-thread CTA with 16K-pair tiles measured 9 % slower
 constexpr int kBinTile = kBinThreads * kBinPPT;    // 8192 pairs per tile
 constexpr int kBinRankBits = 14;                   // key = bin << 14 | rank within the tile
 constexpr int kApplyThreads = 256;
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
 // counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
 // shared-memory counting sort, then the runs written out.
 template <bool PREFIX>
-__global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const __grid_constant__ Geo G,
+__global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ src,
                                                              const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,

@@ -621,7 +621,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     while ((1u << lg) < cfg->g) ++lg;
     B.bpc_log2 = lg - B.s;
     B.nbins = h->G.n_cs << B.bpc_log2;
-    B.nblk = (uint32_t)h->sms * 2;
+    B.nblk = (uint32_t)h->sms * kBinMinBlocks;
     B.ncols = h->G.cs_words / h->G.wpc;
     // scatter tables ≤ 48 KiB (≥ 2 pairs per bin in an 8192-pair tile), word group ≤ 112 KiB
     h->binnable = B.nbins <= 4096 && B.ncols <= 28672;
