@@ -472,7 +472,9 @@ def main():
     if binned:
         # binned update (binned.cuh): algorithmic DRAM bytes of each kernel per launch
         nb = ncu_binned()
-        algo = {"k_bin_count": 8 * n, "k_bin_starts": 3 * 4 * 4096, "k_bin_scatter": 12 * n,
+        # scatter kernel: tile sort k_bin_scatter unless CBAA_BIN_SCATTER=wc (the library's rule)
+        scat = "k_bin_wc" if os.environ.get("CBAA_BIN_SCATTER") == "wc" else "k_bin_scatter"
+        algo = {"k_bin_count": 8 * n, "k_bin_starts": 5 * 4 * 4096, scat: 12 * n,
                 "k_bin_apply": 4 * n + cb.nbytes}
         kernels = {}
         for name, t in zip(algo, per_call):
@@ -484,7 +486,7 @@ def main():
         kd = kernels[dom]
         roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
                     "frac": kd["frac_hbm"], "traffic": kd["ncu_dram_bytes"],
-                    "algorithmic": {"k_bin_count": "8 B/pair read", "k_bin_scatter": "8 B/pair read + 4 B/pair entry "
+                    "algorithmic": {"k_bin_count": "8 B/pair read", scat: "8 B/pair read + 4 B/pair entry "
                                     "written", "k_bin_apply": "4 B/pair entry read + the cube's words OR-ed once"},
                     "per_launch_ms": kd["ms"], "timing": "CUDA event pair around every update kernel on its launch "
                     "stream over the timed region (cbaa_set_phase_timing), averaged per update call",

@@ -10,6 +10,7 @@
 //                  cursor (one atomic per tile and bin), so every bin region fills front to back and L2
 //                  only ever holds one partial line per bin                     reads 8, writes 4 B/pair
 //                  entry = LP << s | (row mod 2^s), s = min(5, r) (fits 32 bits since |LP| = 32 − r)
+//                  (CBAA_BIN_SCATTER=wc: k_bin_wc, per-bin 32-B write-combining slots in shared memory instead)
 //   k_bin_apply    one CTA per word group: the bits are set in a shared-memory image of the group
 //                  (test-and-set, ATOMS.OR only when the bit is still 0), then OR-ed into the cube with
 //                  one RED per non-zero word                                      reads 4 B/pair
@@ -45,6 +46,12 @@ constexpr int kBinRankBits = 14;                   // key = bin << 14 | rank wit
 constexpr int kApplyThreads = 256;
 constexpr int kApplyUnroll = 8;                    // entries per thread in flight
 constexpr int kCountThreads = 1024;
+#ifndef CBAA_CUR_STRIDE
+#define CBAA_CUR_STRIDE 1
+#endif
+// bin b's write cursor is cursor[b · kCurStride]: one 128-B line per cursor, so the scatter's
+// reservation atomics on different bins never queue behind each other in one L2 line
+constexpr uint32_t kCurStride = CBAA_CUR_STRIDE;
 
 template <bool PREFIX>
 __device__ __forceinline__ bool pair_bin(const Geo& G, const BinGeo& B, uint32_t iip, uint32_t oip, uint32_t& bin,
@@ -124,17 +131,21 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_count(const __grid_consta
   }
 }
 
-// Phase 2: start[b] = Σ_{b' < b} counts[b'], start[nbins] = total; cursor := start; counts := 0 for the
-// next round.  One CTA (nbins ≤ 16384).
+// Phase 2: bin regions.  start[b] = Σ_{b' < b} align8(counts[b'] + slack) (sector-aligned; slack = the
+// duplicate padding k_bin_wc may add, 8 entries per CTA), start[nbins] = total, cursor := start (the
+// scatter's bump allocator; the apply reads [start[b], cursor[b])), counts := 0 for the next round, the
+// overflow-log count := 0.  One CTA (nbins ≤ 16384).
 constexpr int kStartThreads = 1024;
-__global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t* __restrict__ counts,
+__global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t slack,
+                                                              uint32_t* __restrict__ counts,
                                                               uint32_t* __restrict__ start,
-                                                              uint32_t* __restrict__ cursor) {
+                                                              uint32_t* __restrict__ cursor,
+                                                              uint32_t* __restrict__ log_n) {
   __shared__ uint32_t s_w[kStartThreads / 32];
   const uint32_t per = (nbins + kStartThreads - 1) / kStartThreads;
   const uint32_t b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
   uint32_t loc = 0;
-  for (uint32_t b = b0; b < b1; ++b) loc += counts[b];
+  for (uint32_t b = b0; b < b1; ++b) loc += (counts[b] + slack + 7u) & ~7u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = loc;
 #pragma unroll
@@ -152,15 +163,18 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
   for (uint32_t b = b0; b < b1; ++b) {
     const uint32_t x = counts[b];
     start[b] = run;
-    cursor[b] = run;
+    cursor[b * kCurStride] = run;
     counts[b] = 0;
-    run += x;
+    run += (x + slack + 7u) & ~7u;
   }
-  if (threadIdx.x == 0) start[nbins] = tot;
+  if (threadIdx.x == 0) {
+    start[nbins] = tot;
+    *log_n = 0;
+  }
 }
 
-// Phase 3: entries of CTA j's chunk, tile by tile: rank within the tile by ATOMS on the tile's bin
-// counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
+// Phase 3 (default): entries of CTA j's chunk, tile by tile: rank within the tile by ATOMS on
+// the tile's bin counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
 // shared-memory counting sort, then the runs written out.
 template <bool PREFIX>
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(const __grid_constant__ Geo G,
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
           x[j] = (i0 + 32 * j < wchunk && b < B.nbins) ? toff[b] : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + w0 + i0 + 32 * j + lane, x[j]) : 0u;
+        for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + (w0 + i0 + 32 * j + lane) * kCurStride, x[j]) : 0u;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (x[j]) base[w0 + i0 + 32 * j + lane] = r[j];
@@ -290,6 +304,169 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
   }
 }
 
+// Column of array a for LP (P:235 RA: CL_bs window of LP; P:239 VA: H_j(LP)).
+__device__ __forceinline__ uint32_t lp_col(const Geo& G, uint64_t dbl, uint32_t lp, uint32_t a) {
+  return a < G.num_ra ? (uint32_t)(dbl >> G.sh[a]) & G.colmask[a]
+                      : mix32(lp ^ G.va_seeds[a - G.num_ra]) & G.colmask[a];
+}
+
+// Phase 3 (CBAA_BIN_SCATTER=wc): write-combining scatter.  One 1024-thread CTA per SM streams its chunk in rounds of
+// kWcRound pairs.  Every bin owns a kWcSlot-entry slot in shared memory; a pair is appended to its bin's
+// slot (rank by ATOMS on the bin's fill count).  After a barrier, thread t owns bins 4t..4t+3: a slot
+// holding ≥ 8 entries stores its first 8 to the bin's region as one 32-B sector, at a position reserved
+// by a global atomic issued when the bin's previous sector was stored (so the reservation's latency
+// overlaps a round of appends), and moves its tail to the front.  The 4 spare entries per slot make an
+// append that finds its slot full rare (≥ 5 more appends to one bin in a round than the slot has room
+// for); such appends go to an overflow log that k_bin_log applies with the direct update's test-and-set.
+// When the CTA ends, each bin's pending reservation (or a fresh one) takes its partial slot, padded with
+// duplicates of one of the bin's entries: OR is idempotent, so duplicates change nothing in the cube.  A
+// region therefore needs counts[b] + 8 slots per CTA (k_bin_starts); the apply reads [start[b], cursor[b]).
+constexpr int kWcThreads = 1024;
+constexpr int kWcPPT = 4;                          // pairs per thread per round (one 16-B load per array)
+constexpr int kWcRound = kWcThreads * kWcPPT;      // 4096 pairs per round
+constexpr uint32_t kWcSlot = 12;                   // entries per slot (a sector + 4 spare)
+__host__ __device__ constexpr size_t wc_smem_bytes(uint32_t nbins) { return (size_t)nbins * (4 * kWcSlot + 4); }
+__device__ __forceinline__ uint4 lds4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+__device__ __forceinline__ void sts(uint32_t a, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ void st_sector(uint32_t* p, uint4 a, uint4 b) {
+  reinterpret_cast<uint4*>(p)[0] = a;
+  reinterpret_cast<uint4*>(p)[1] = b;
+}
+__device__ __forceinline__ uint32_t get4(const uint4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+
+template <bool PREFIX>
+__global__ void __launch_bounds__(kWcThreads, 1) k_bin_wc(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
+                                                          const uint32_t* __restrict__ src,
+                                                          const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
+                                                          int vec, uint32_t* __restrict__ cursor,
+                                                          uint32_t* __restrict__ entries, uint32_t* __restrict__ log_n,
+                                                          uint32_t* __restrict__ log_e, uint16_t* __restrict__ log_b) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* occ = sm + kWcSlot * B.nbins;                           // [nbins] fill counts; slot of bin b: sm[12·b ..]
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t b = tid; b < B.nbins; b += kWcThreads) occ[b] = 0;
+  const uint32_t slot_sa = pin(smem_addr(sm)), occ_sa = pin(smem_addr(occ));
+  const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), pgm = pin(G.g - 1u);
+  const uint32_t prm = pin(G.rmask), pr = pin(G.r), pbl = pin(B.bpc_log2), pes = pin(B.s);
+  const uint32_t psm = pin((1u << B.s) - 1u);
+  const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
+  const uint32_t b0 = 4u * tid;                                     // owned bins b0..b0+3
+  const bool owner = b0 < B.nbins;
+  uint32_t res[4] = {0u, 0u, 0u, 0u}, rep[4] = {0u, 0u, 0u, 0u}, hasres = 0;
+  uint32_t ca[kWcPPT], cb[kWcPPT];
+  bool cin[kWcPPT];
+  load_quad(src, dst, c0 + 4ull * tid, c1, vec, ca, cb, cin);
+  __syncthreads();
+  for (uint64_t t0 = c0; t0 < c1; t0 += kWcRound) {
+    const uint64_t t1 = t0 + kWcRound;
+    uint32_t ab[kWcPPT], ae[kWcPPT], r[kWcPPT];
+    bool av[kWcPPT];
+#pragma unroll
+    for (int i = 0; i < kWcPPT; ++i) {
+      uint32_t bin = 0, e = 0;
+      bool ok = cin[i];
+      if (PREFIX) {
+        ok = ok && pair_bin<true>(G, B, ca[i], cb[i], bin, e);
+      } else {
+        const uint32_t mi = pa * ca[i] + pb, mo = pa * cb[i] + pb;           // P:175, Q2
+        const uint32_t row = mix32(mo ^ pbv) & pgm;
+        bin = ((mi & prm) << pbl) | (row >> pes);                           // (cs, row >> s)
+        e = ((mi >> pr) << pes) | (row & psm);                              // LP, low row bits
+      }
+      ab[i] = bin, ae[i] = e, av[i] = ok;
+    }
+#pragma unroll
+    for (int i = 0; i < kWcPPT; ++i) r[i] = av[i] ? atoms_inc(occ_sa + 4u * ab[i]) : kWcSlot;
+#pragma unroll
+    for (int i = 0; i < kWcPPT; ++i) {
+      if (r[i] < kWcSlot) {
+        sts(slot_sa + 4u * (kWcSlot * ab[i] + r[i]), ae[i]);
+      } else if (av[i]) {
+        const uint32_t k = atomicAdd(log_n, 1u);
+        log_e[k] = ae[i];
+        log_b[k] = (uint16_t)ab[i];
+      }
+    }
+    __syncthreads();
+    // flush the owned slots holding a sector
+    if (owner) {
+      uint4 o = lds4(occ_sa + 4u * b0);
+      const uint32_t had = hasres;
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {   // unrolled: res[k] is written by its atomic directly, never waited on
+        const uint32_t m = get4(o, k), b = b0 + k;
+        if (m >= 8u) {
+          const uint32_t sa = slot_sa + 4u * kWcSlot * b;
+          const uint4 v0 = lds4(sa), v1 = lds4(sa + 16u), v2 = lds4(sa + 32u);
+          const uint32_t pos = (had >> k) & 1u ? res[k] : atomicAdd(cursor + b * kCurStride, 8u);
+          st_sector(entries + pos, v0, v1);
+          sts4(sa, v2);                         // tail (entries 8..11) to the front
+          rep[k] = v0.x;
+          any = true;
+        }
+        // the next sector's position, used a round or more later: reserved after every stored sector, and
+        // first when the slot is half full, so no flush waits on its atomic; a predicated atomic into res[k]
+        // itself (a pending reservation always meets ≥ 4 entries or a stored sector at the end, so it can
+        // always be filled)
+        const uint32_t want = (m >= 8u || (m >= 4u && !((had >> k) & 1u))) ? 1u : 0u;
+        asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p atom.global.add.u32 %0, [%1], %3;\n}"
+                     : "+r"(res[k]) : "l"(cursor + b * kCurStride), "r"(want), "r"(8u) : "memory");
+        hasres |= want << k;
+      }
+      if (any) {
+        o.x = o.x >= 8u ? min(o.x, kWcSlot) - 8u : o.x, o.y = o.y >= 8u ? min(o.y, kWcSlot) - 8u : o.y;
+        o.z = o.z >= 8u ? min(o.z, kWcSlot) - 8u : o.z, o.w = o.w >= 8u ? min(o.w, kWcSlot) - 8u : o.w;
+        sts4(occ_sa + 4u * b0, o);
+      }
+    }
+    load_quad(src, dst, t1 + 4ull * tid, c1, vec, ca, cb, cin);   // next round's pairs (after the flush)
+    __syncthreads();
+  }
+  // partial slots: into the pending reservation (or a fresh sector), padded with duplicates
+  if (owner) {
+    const uint4 o = lds4(occ_sa + 4u * b0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t m = get4(o, k), b = b0 + k, has = (hasres >> k) & 1u;
+      if (!m && !has) continue;
+      const uint32_t pos = has ? res[k] : atomicAdd(cursor + b * kCurStride, 8u);
+      uint32_t v[8];
+      const uint32_t fill = m ? sm[kWcSlot * b] : rep[k];
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) v[i] = i < m ? sm[kWcSlot * b + i] : fill;
+      st_sector(entries + pos, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]));
+    }
+  }
+}
+
+// Overflow log of k_bin_wc (appends that found their bin's slot full): each record sets its pair's bits in
+// the cube with the direct update's test-and-set (L1-cached load, RED only for a clear bit; §6), so
+// the repeated records of a heavy flow cost loads, not atomics.
+__global__ void k_bin_log(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
+                          const uint32_t* __restrict__ log_n, const uint32_t* __restrict__ log_e,
+                          const uint16_t* __restrict__ log_b, uint32_t* __restrict__ cube) {
+  const uint32_t nrec = *log_n;
+  const uint32_t smask = (1u << B.s) - 1u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+    const uint32_t bin = log_b[i], e = log_e[i];
+    const uint32_t cs = bin >> B.bpc_log2, row = ((bin & ((1u << B.bpc_log2) - 1u)) << B.s) | (e & smask);
+    const uint32_t lp = e >> B.s, bit = 1u << (row & 31u);
+    const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+    for (uint32_t a = 0; a < G.narr; ++a) {
+      uint32_t* w = cube + (uint64_t)cs * G.cs_words + G.arr_off[a] + (uint64_t)lp_col(G, dbl, lp, a) * G.wpc + (row >> 5);
+      if (!(__ldca(w) & bit)) red_or(w, bit);
+    }
+  }
+}
+
 // Shared-memory test-and-set pieces of k_bin_apply, on 32-bit shared addresses.  A load may see a stale
 // 0 (the bit set by another thread meanwhile): that only costs a redundant RED, never a lost bit.
 __device__ __forceinline__ uint32_t lds(uint32_t a) {
@@ -301,12 +478,6 @@ __device__ __forceinline__ void reds_or(uint32_t a, uint32_t bit) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit));
 }
 
-// Column of array a for LP (P:235 RA: CL_bs window of LP; P:239 VA: H_j(LP)).
-__device__ __forceinline__ uint32_t lp_col(const Geo& G, uint64_t dbl, uint32_t lp, uint32_t a) {
-  return a < G.num_ra ? (uint32_t)(dbl >> G.sh[a]) & G.colmask[a]
-                      : mix32(lp ^ G.va_seeds[a - G.num_ra]) & G.colmask[a];
-}
-
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the
 // group (word i = word w of column i of CS cs, columns of all arrays in S:116 order), which is then
 // OR-ed into the cube.  The CTA owns those words for the whole launch.  <3, 1>: paper shape unrolled.
@@ -314,6 +485,7 @@ template <int NRA, int NVA, int S>
 __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ start,
+                                                             const uint32_t* __restrict__ end,
                                                              const uint32_t* __restrict__ entries,
                                                              uint32_t* __restrict__ cube) {
   // S: entry row bits known at compile time (4 = the paper's r = 4, hence also L = 28), −1: run time
@@ -331,7 +503,9 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
   const uint32_t es = S >= 0 ? (uint32_t)S : B.s;
   const uint32_t L = (S >= 0 && S < 5) ? 32u - (uint32_t)S : G.L;   // s < 5 ⇔ r = s
   const uint32_t kb = 1u << (5 - es), b0 = (cs << B.bpc_log2) + w * kb, smask = (1u << es) - 1u;
+  // bin k of the group holds [start[b0 + k], end[b0 + k]); the sector padding up to start[b0 + k + 1] is skipped
   const uint32_t P0 = start[b0], P1 = start[b0 + kb], B1 = pin(kb > 1 ? start[b0 + 1] : P1);
+  const uint32_t E0 = pin(end[b0 * kCurStride]), E1 = pin(kb > 1 ? end[(b0 + 1) * kCurStride] : E0);
   // paper shape: per-array shift, mask and shared base address pinned in registers
   uint32_t shv[NRA > 0 ? NRA : 1], mk[NRA > 0 ? NRA + NVA : 1], ab[NRA > 0 ? NRA + NVA : 1];
   uint32_t vseed = 0;
@@ -346,9 +520,17 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
   }
   auto apply_one = [&](uint32_t e, uint32_t q) {
     uint32_t hi = 0;
-    if (kb == 2) hi = q >= B1 ? 1u << es : 0u;
-    else if (kb > 2)
-      for (uint32_t k = 1; k < kb; ++k) hi += q >= start[b0 + k] ? 1u << es : 0u;
+    if (kb == 1) {
+      if (q >= E0) return;
+    } else if (kb == 2) {
+      hi = q >= B1 ? 1u << es : 0u;
+      if (q >= (hi ? E1 : E0)) return;
+    } else {
+      uint32_t k = 0;
+      for (uint32_t j = 1; j < kb; ++j) k += q >= start[b0 + j] ? 1u : 0u;
+      if (q >= end[(b0 + k) * kCurStride]) return;
+      hi = k << es;
+    }
     const uint32_t lp = e >> es, bit = 1u << (hi | (e & smask));
     const uint64_t dbl = ((uint64_t)lp << L) | lp;
     if constexpr (NRA > 0) {

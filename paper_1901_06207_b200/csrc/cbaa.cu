@@ -79,7 +79,9 @@ struct cbaa_handle {
   uint64_t bin_chunk = 1ull << 28;   // pairs per count/scatter/apply round (CBAA_BIN_CHUNK, tests)
   uint32_t* bin_ent = nullptr;
   uint64_t bin_cap = 0;
-  uint32_t* bin_tab = nullptr;    // counts | start | cursor
+  uint32_t* bin_tab = nullptr;    // counts | start | cursor | log count
+  void* bin_log = nullptr;        // k_bin_wc overflow log
+  int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
   // per-kernel update timing (cbaa_set_phase_timing)
   int timing = 0;
   std::vector<cudaEvent_t> tev;   // pairs: tev[2k], tev[2k+1]
@@ -428,24 +430,33 @@ void t_end(cbaa_handle* h, int k, cudaStream_t s) {
 int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t kChunk = h->bin_chunk;
   const BinGeo& B = h->B;
-  const uint64_t want = std::min(n, kChunk);
+  // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
+  const uint32_t slack = 8u * (uint32_t)h->sms;
+  const uint64_t want = std::min(n, kChunk) + (uint64_t)(slack + 8) * B.nbins;
   if (h->bin_cap < want) {
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
     h->bin_ent = nullptr;
     h->bin_cap = 0;
     CK(h, cudaMalloc(&h->bin_ent, want * 4));
     h->bin_cap = want;
+    if (h->bin_log) CK(h, cudaFree(h->bin_log));
+    h->bin_log = nullptr;
+    CK(h, cudaMalloc(&h->bin_log, std::min(n, kChunk) * 6 + 16));   // overflow log: u32 entries | u16 bins
   }
-  if (!h->bin_tab) {   // counts [nbins] | start [nbins + 1] | cursor [nbins]
-    CK(h, cudaMalloc(&h->bin_tab, (3ull * B.nbins + 1) * 4));
+  if (!h->bin_tab) {   // counts [nbins] | start [nbins + 1] | cursor [nbins · kCurStride] | log count
+    CK(h, cudaMalloc(&h->bin_tab, ((2ull + kCurStride) * B.nbins + 2) * 4));
     CK(h, cudaMemsetAsync(h->bin_tab, 0, (uint64_t)B.nbins * 4, s));
   }
   uint32_t* counts = h->bin_tab;
   uint32_t* start = counts + B.nbins;
   uint32_t* cursor = start + B.nbins + 1;
+  uint32_t* log_n = cursor + (uint64_t)B.nbins * kCurStride;
+  uint32_t* log_e = reinterpret_cast<uint32_t*>(h->bin_log);
+  uint16_t* log_b = reinterpret_cast<uint16_t*>(log_e + std::min(n, kChunk));
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
   const size_t sm_cnt = (size_t)B.nbins * 4;
   const size_t sm_sc = (size_t)(2 * B.nbins + 1) * 4 + (size_t)kBinTile * 6;
+  const size_t sm_wc = wc_smem_bytes(B.nbins);
   const size_t sm_ap = (size_t)B.ncols * 4;
   const uint32_t n_wg = h->G.n_cs * h->G.wpc;
   for (uint64_t off = 0; off < n; off += kChunk) {
@@ -463,23 +474,36 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     int rc = launch_check(h, "k_bin_count");
     if (rc) return rc;
     tk = t_begin(h, 1, s);
-    k_bin_starts<<<1, kStartThreads, 0, s>>>(B.nbins, counts, start, cursor);
+    k_bin_starts<<<1, kStartThreads, 0, s>>>(B.nbins, slack, counts, start, cursor, log_n);
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_starts"))) return rc;
     tk = t_begin(h, 2, s);
-    if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
-    else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+    if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
+      const uint32_t nw = (uint32_t)h->sms;
+      const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
+      if (prefix)
+        k_bin_wc<true><<<nw, kWcThreads, sm_wc, s>>>(h->G, B, a, b, m, per_w, vec, cursor, h->bin_ent, log_n, log_e, log_b);
+      else
+        k_bin_wc<false><<<nw, kWcThreads, sm_wc, s>>>(h->G, B, a, b, m, per_w, vec, cursor, h->bin_ent, log_n, log_e, log_b);
+    } else {           // tile counting sort (default)
+      if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+      else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+    }
     t_end(h, tk, s);
-    if ((rc = launch_check(h, "k_bin_scatter"))) return rc;
+    if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
     tk = t_begin(h, 3, s);
     if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
-      k_bin_apply<3, 1, 4><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+      k_bin_apply<3, 1, 4><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else if (h->G.num_ra == 3 && h->G.num_va == 1)
-      k_bin_apply<3, 1, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+      k_bin_apply<3, 1, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else
-      k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, h->bin_ent, h->cube);
+      k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
+    if (h->bin_wc) {   // the scatter's overflow log (usually empty: the kernel exits at once)
+      k_bin_log<<<h->sms, 256, 0, s>>>(h->G, B, log_n, log_e, log_b, h->cube);
+      if ((rc = launch_check(h, "k_bin_log"))) return rc;
+    }
   }
   return CBAA_OK;
 }
@@ -640,6 +664,11 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((2 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
       cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      const char* bs = std::getenv("CBAA_BIN_SCATTER");
+      h->bin_wc = bs && std::strcmp(bs, "wc") == 0;
+      const int sm_wc = (int)wc_smem_bytes(B.nbins);
+      cudaFuncSetAttribute(k_bin_wc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
+      cudaFuncSetAttribute(k_bin_wc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
       cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -667,6 +696,7 @@ void cbaa_destroy(cbaa_handle* h) {
   if (h->scratch) cudaFree(h->scratch);
   if (h->bin_ent) cudaFree(h->bin_ent);
   if (h->bin_tab) cudaFree(h->bin_tab);
+  if (h->bin_log) cudaFree(h->bin_log);
   for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
   if (h->prefix_bits) cudaFree(h->prefix_bits);
   if (h->D.cand) cudaFree(h->D.cand);

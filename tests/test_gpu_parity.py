@@ -571,3 +571,30 @@ def test_binned_c2_full_size(paper):
     w = W.generate(W.C2, 1, with_raw=False)
     cb, ref, hosts, stats = full_check(paper, w.src, w.dst, 1024, update_mode=2)
     assert 550 <= len(hosts) <= 750
+
+
+@pytest.mark.parametrize("scatter", ["wc", "tile"])
+def test_binned_scatter_variants(paper, scatter, monkeypatch):
+    """Both scatters (write-combining slots with overflow re-append and back-cursor spill, and the tile
+    counting sort) produce the oracle's cube: a ragged Zipf window with planted hosts, one pair repeated
+    400K times (every slot overflows, the overflow list fills, the back-cursor path runs), and a window
+    whose pairs fall in a handful of bins."""
+    monkeypatch.setenv("CBAA_BIN_SCATTER", scatter)
+    spec = W.WindowSpec(n=700_001, n_hosts=20_000, n_flows=150_000, card_cap=400, scanners=(2000, 1500),
+                        victims=(2500,))
+    w = W.generate(spec, 41)
+    full_check(paper, w.src, w.dst, 1024, **BIN)
+    n = 400_000
+    src = np.full(n, 0x0A000001, np.uint32)
+    dst = np.full(n, 0x08080808, np.uint32)
+    cb = handle(paper, **BIN)
+    cb.reset()
+    cb.update(dev(src), dev(dst))
+    ref, _ = O.update(paper, src[:1], dst[:1])
+    assert np.array_equal(gpu_cube(cb), ref)
+    s3 = np.full(n, 0x0A000003, np.uint32)
+    d3 = (np.arange(n, dtype=np.uint32) % 7) + 0x30000000
+    cb.reset()
+    cb.update(dev(s3), dev(d3))
+    ref, _ = O.update(paper, s3[:7], d3[:7])
+    assert np.array_equal(gpu_cube(cb), ref)
