@@ -131,12 +131,47 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_count(const __grid_consta
   }
 }
 
-// Phase 2: bin regions.  start[b] = Σ_{b' < b} align8(counts[b'] + slack) (sector-aligned; slack = the
-// duplicate padding k_bin_wc may add, 8 entries per CTA), start[nbins] = total, cursor := start (the
-// scatter's bump allocator; the apply reads [start[b], cursor[b])), counts := 0 for the next round, the
-// overflow-log count := 0.  One CTA (nbins ≤ 16384).
+// Phase 1, sampled (default for large normalised windows): the histogram of every 2^L-th block of
+// kSampleBlk pairs only (1/16 of the input); k_bin_starts scales it up with a safety margin.  A region
+// that still turns out too small spills its excess entries to the overflow log (k_bin_log), so the cube
+// is exact for any input — the sample only decides how much of the work takes the fast path.
+constexpr uint32_t kSampleBlk = 4u * kCountThreads;   // 4096 pairs, one 16-B quad per thread
+__global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
+                                                            const uint32_t* __restrict__ src,
+                                                            const uint32_t* __restrict__ dst, uint64_t n,
+                                                            uint32_t stride_log2, int vec, uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t hist[];
+  for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads) hist[b] = 0;
+  __syncthreads();
+  const uint64_t nblk = (n + kSampleBlk - 1) / kSampleBlk;
+  for (uint64_t sb = blockIdx.x; (sb << stride_log2) < nblk; sb += gridDim.x) {
+    const uint64_t k0 = (sb << stride_log2) * kSampleBlk, c1 = min(n, k0 + kSampleBlk);
+    uint32_t ss[4], dd[4];
+    bool in[4];
+    load_quad(src, dst, k0 + 4ull * threadIdx.x, c1, vec, ss, dd, in);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t bin, ent;
+      if (in[e] && pair_bin<false>(G, B, ss[e], dd[e], bin, ent)) atomicAdd(&hist[bin], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads)
+    if (hist[b]) atomicAdd(counts + b, hist[b]);
+}
+
+// Phase 2: bin regions.  start[b] = Σ_{b' < b} cap(b') with cap(b) = align8(counts[b] + slack) for exact
+// counts (sector-aligned; slack = the duplicate padding k_bin_wc may add, 8 entries per CTA), or, for a
+// 1/2^L sample, the scaled count est = counts[b]·2^L plus est/4 + 64; start[nbins] = total, cursor :=
+// start (the scatter's bump allocator; the apply reads [start[b], min(cursor[b], start[b + 1]))),
+// counts := 0 for the next round, the overflow-log count := 0.  One CTA (nbins ≤ 16384).
 constexpr int kStartThreads = 1024;
-__global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t slack,
+__device__ __forceinline__ uint32_t bin_cap(uint32_t c, uint32_t slack, uint32_t sample_log2) {
+  if (!sample_log2) return (c + slack + 7u) & ~7u;
+  const uint32_t est = c << sample_log2;
+  return (est + est / 4u + 64u + slack + 7u) & ~7u;
+}
+__global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t slack, uint32_t sample_log2,
                                                               uint32_t* __restrict__ counts,
                                                               uint32_t* __restrict__ start,
                                                               uint32_t* __restrict__ cursor,
@@ -145,7 +180,7 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
   const uint32_t per = (nbins + kStartThreads - 1) / kStartThreads;
   const uint32_t b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
   uint32_t loc = 0;
-  for (uint32_t b = b0; b < b1; ++b) loc += (counts[b] + slack + 7u) & ~7u;
+  for (uint32_t b = b0; b < b1; ++b) loc += bin_cap(counts[b], slack, sample_log2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = loc;
 #pragma unroll
@@ -165,7 +200,7 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
     start[b] = run;
     cursor[b * kCurStride] = run;
     counts[b] = 0;
-    run += (x + slack + 7u) & ~7u;
+    run += bin_cap(x, slack, sample_log2);
   }
   if (threadIdx.x == 0) {
     start[nbins] = tot;
@@ -182,15 +217,21 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
                                                              const uint32_t* __restrict__ src,
                                                              const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
                                                              int vec, uint32_t* __restrict__ cursor,
-                                                             uint32_t* __restrict__ entries) {
+                                                             uint32_t* __restrict__ entries,
+                                                             const uint32_t* __restrict__ start,
+                                                             uint32_t* __restrict__ log_n, uint32_t* __restrict__ log_e,
+                                                             uint16_t* __restrict__ log_b) {
   extern __shared__ uint32_t sm[];
   uint32_t* base = sm;                                   // [nbins] this tile's reserved slot of each bin
   uint32_t* toff = base + B.nbins;                       // [nbins + 1] tile counts → exclusive offsets
   uint32_t* stage = toff + B.nbins + 1;                  // [kBinTile] entries sorted by bin
   uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kBinTile);   // [kBinTile] their bins
+  uint32_t* rend = reinterpret_cast<uint32_t*>(sbin + kBinTile);    // [nbins] region ends start[b + 1]
   __shared__ uint32_t s_w[kBinThreads / 32];
+  __shared__ int s_ovf;                                  // some run of this tile passes its region's end
   const uint32_t tid = threadIdx.x;
-  for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
+  for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
+  if (tid == 0) s_ovf = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t wchunk = (B.nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
   const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), pgm = pin(G.g - 1u);
@@ -250,11 +291,16 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + (w0 + i0 + 32 * j + lane) * kCurStride, x[j]) : 0u;
+        bool over = false;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          if (x[j]) base[w0 + i0 + 32 * j + lane] = r[j];
+          if (x[j]) {
+            base[w0 + i0 + 32 * j + lane] = r[j];
+            over |= r[j] + x[j] > rend[w0 + i0 + 32 * j + lane];
+          }
           loc += x[j];
         }
+        if (over) s_ovf = 1;
       }
       uint32_t incl = loc;
 #pragma unroll
@@ -295,11 +341,23 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
     }
     __syncthreads();
     const uint32_t total = toff[B.nbins];
-    for (uint32_t p = tid; p < total; p += kBinThreads) {
-      entries[base[sbin[p]] + p] = stage[p];
+    if (!s_ovf) {
+      for (uint32_t p = tid; p < total; p += kBinThreads) entries[base[sbin[p]] + p] = stage[p];
+    } else {   // entries past their region's end (a sampled capacity fell short) go to the overflow log
+      for (uint32_t p = tid; p < total; p += kBinThreads) {
+        const uint32_t bin = sbin[p], g = base[bin] + p;
+        if (g < rend[bin]) {
+          entries[g] = stage[p];
+        } else {
+          const uint32_t k = atomicAdd(log_n, 1u);
+          log_e[k] = stage[p];
+          log_b[k] = (uint16_t)bin;
+        }
+      }
     }
     __syncthreads();
     for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
+    if (tid == 0) s_ovf = 0;
     __syncthreads();
   }
 }
@@ -498,14 +556,16 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
 #pragma unroll
   for (uint32_t a = 0; a < CBAA_MAX_ARRAYS; ++a) cbase[a] = a < narr ? G.arr_off[a] >> G.wpc_log2 : 0u;
   __syncthreads();
-  // the word group's bins are adjacent in the entry array: one range [P0, P1), bin k of the group gives
-  // row bits k << s; loads of the next batch are issued before the current batch is applied
+  // the word group's bins are adjacent in the entry array, bin k of the group gives row bits k << s;
+  // loads of the next batch are issued before the current batch is applied
   const uint32_t es = S >= 0 ? (uint32_t)S : B.s;
   const uint32_t L = (S >= 0 && S < 5) ? 32u - (uint32_t)S : G.L;   // s < 5 ⇔ r = s
   const uint32_t kb = 1u << (5 - es), b0 = (cs << B.bpc_log2) + w * kb, smask = (1u << es) - 1u;
-  // bin k of the group holds [start[b0 + k], end[b0 + k]); the sector padding up to start[b0 + k + 1] is skipped
+  // bin k of the group holds [start[b0 + k], min(cursor, start[b0 + k + 1])); the rest of its region (sector
+  // padding, unused capacity) is skipped, and a cursor past the region's end means the excess is in the log
   const uint32_t P0 = start[b0], P1 = start[b0 + kb], B1 = pin(kb > 1 ? start[b0 + 1] : P1);
-  const uint32_t E0 = pin(end[b0 * kCurStride]), E1 = pin(kb > 1 ? end[(b0 + 1) * kCurStride] : E0);
+  const uint32_t E0 = pin(min(end[b0 * kCurStride], start[b0 + 1]));
+  const uint32_t E1 = pin(kb > 1 ? min(end[(b0 + 1) * kCurStride], start[b0 + 2]) : E0);
   // paper shape: per-array shift, mask and shared base address pinned in registers
   uint32_t shv[NRA > 0 ? NRA : 1], mk[NRA > 0 ? NRA + NVA : 1], ab[NRA > 0 ? NRA + NVA : 1];
   uint32_t vseed = 0;
@@ -518,17 +578,21 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
     }
     if constexpr (NVA == 1) vseed = pin(G.va_seeds[0]);
   }
-  auto apply_one = [&](uint32_t e, uint32_t q) {
+  // kb ≤ 2 (r ≥ 4, the paper's geometry): the valid entries of the group's bins are walked as one
+  // virtual range [0, len0 + len1) — bin 0's then bin 1's — so no padding or spare capacity is read;
+  // kb > 2: positions [P0, P1) with a per-entry bin search and validity check
+  const uint32_t len0 = E0 - P0, len1 = kb == 2 ? E1 - B1 : 0u;
+  const uint32_t V = kb <= 2 ? len0 + len1 : P1 - P0;
+  auto at = [&](uint32_t v) -> uint32_t { return kb <= 2 ? (v < len0 ? P0 + v : B1 + (v - len0)) : P0 + v; };
+  auto apply_one = [&](uint32_t e, uint32_t v) {
     uint32_t hi = 0;
-    if (kb == 1) {
-      if (q >= E0) return;
-    } else if (kb == 2) {
-      hi = q >= B1 ? 1u << es : 0u;
-      if (q >= (hi ? E1 : E0)) return;
-    } else {
+    if (kb == 2) {
+      hi = v >= len0 ? 1u << es : 0u;
+    } else if (kb > 2) {
+      const uint32_t q = P0 + v;
       uint32_t k = 0;
       for (uint32_t j = 1; j < kb; ++j) k += q >= start[b0 + j] ? 1u : 0u;
-      if (q >= end[(b0 + k) * kCurStride]) return;
+      if (q >= min(end[(b0 + k) * kCurStride], start[b0 + k + 1])) return;
       hi = k << es;
     }
     const uint32_t lp = e >> es, bit = 1u << (hi | (e & smask));
@@ -554,22 +618,22 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
   };
   constexpr uint32_t kStep = kApplyUnroll * kApplyThreads;
   uint32_t e[kApplyUnroll];
-  uint32_t p = P0 + threadIdx.x;
+  uint32_t p = threadIdx.x;
 #pragma unroll
-  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kApplyThreads < P1 ? __ldcs(entries + p + u * kApplyThreads) : 0u;
-  while (p < P1) {
+  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kApplyThreads < V ? __ldcs(entries + at(p + u * kApplyThreads)) : 0u;
+  while (p < V) {
     const uint32_t pn = p + kStep;
     uint32_t en[kApplyUnroll];
 #pragma unroll
     for (int u = 0; u < kApplyUnroll; ++u)
-      en[u] = pn + u * kApplyThreads < P1 ? __ldcs(entries + pn + u * kApplyThreads) : 0u;
-    if (p + (kApplyUnroll - 1) * kApplyThreads < P1) {   // whole batch: no per-entry bound checks
+      en[u] = pn + u * kApplyThreads < V ? __ldcs(entries + at(pn + u * kApplyThreads)) : 0u;
+    if (p + (kApplyUnroll - 1) * kApplyThreads < V) {   // whole batch: no per-entry bound checks
 #pragma unroll
       for (int u = 0; u < kApplyUnroll; ++u) apply_one(e[u], p + u * kApplyThreads);
     } else {
 #pragma unroll
       for (int u = 0; u < kApplyUnroll; ++u)
-        if (p + u * kApplyThreads < P1) apply_one(e[u], p + u * kApplyThreads);
+        if (p + u * kApplyThreads < V) apply_one(e[u], p + u * kApplyThreads);
     }
 #pragma unroll
     for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];

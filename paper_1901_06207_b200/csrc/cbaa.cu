@@ -82,6 +82,8 @@ struct cbaa_handle {
   uint32_t* bin_tab = nullptr;    // counts | start | cursor | log count
   void* bin_log = nullptr;        // k_bin_wc overflow log
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
+  uint32_t bin_sample_log2 = 4;   // regions sized from a 1/2^L sample (0: exact count; CBAA_BIN_SAMPLE)
+  uint64_t bin_sample_min = 1ull << 24;   // chunks with fewer pairs are counted exactly (CBAA_BIN_SAMPLE_MIN)
   // per-kernel update timing (cbaa_set_phase_timing)
   int timing = 0;
   std::vector<cudaEvent_t> tev;   // pairs: tev[2k], tev[2k+1]
@@ -432,7 +434,16 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   const BinGeo& B = h->B;
   // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
   const uint32_t slack = 8u * (uint32_t)h->sms;
-  const uint64_t want = std::min(n, kChunk) + (uint64_t)(slack + 8) * B.nbins;
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  // sampled region sizing (k_bin_sample): normalised input, tile scatter, chunks of ≥ bin_sample_min pairs
+  const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
+  const uint64_t mx = std::min(n, kChunk);
+  const bool any_sampled = samp && mx >= h->bin_sample_min;
+  // Σ cap(b) ≤ exact: m + nbins·(slack + 7); sampled: 1.25·(m + 2^L·4096) + nbins·(64 + slack + 7)
+  const uint64_t want = std::max<uint64_t>(mx + (uint64_t)(slack + 8) * B.nbins,
+                                           any_sampled ? (mx + ((uint64_t)kSampleBlk << samp)) * 5 / 4 +
+                                                             (uint64_t)(slack + 72) * B.nbins
+                                                       : 0);
   if (h->bin_cap < want) {
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
     h->bin_ent = nullptr;
@@ -453,9 +464,8 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   uint32_t* log_n = cursor + (uint64_t)B.nbins * kCurStride;
   uint32_t* log_e = reinterpret_cast<uint32_t*>(h->bin_log);
   uint16_t* log_b = reinterpret_cast<uint16_t*>(log_e + std::min(n, kChunk));
-  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
   const size_t sm_cnt = (size_t)B.nbins * 4;
-  const size_t sm_sc = (size_t)(2 * B.nbins + 1) * 4 + (size_t)kBinTile * 6;
+  const size_t sm_sc = (size_t)(3 * B.nbins + 1) * 4 + (size_t)kBinTile * 6;
   const size_t sm_wc = wc_smem_bytes(B.nbins);
   const size_t sm_ap = (size_t)B.ncols * 4;
   const uint32_t n_wg = h->G.n_cs * h->G.wpc;
@@ -467,14 +477,19 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     const int vec = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
     const uint32_t nc = 2 * (uint32_t)h->sms;   // count grid: any chunking works (global totals)
     const uint64_t per_c = (((m + nc - 1) / nc) + 3) & ~3ull;
+    const uint32_t sl = samp && m >= h->bin_sample_min ? samp : 0u;
     int tk = t_begin(h, 0, s);
-    if (prefix) k_bin_count<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, h->skipped);
-    else k_bin_count<false><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, nullptr);
+    if (sl)
+      k_bin_sample<<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
+    else if (prefix)
+      k_bin_count<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, h->skipped);
+    else
+      k_bin_count<false><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, nullptr);
     t_end(h, tk, s);
-    int rc = launch_check(h, "k_bin_count");
+    int rc = launch_check(h, sl ? "k_bin_sample" : "k_bin_count");
     if (rc) return rc;
     tk = t_begin(h, 1, s);
-    k_bin_starts<<<1, kStartThreads, 0, s>>>(B.nbins, slack, counts, start, cursor, log_n);
+    k_bin_starts<<<1, kStartThreads, 0, s>>>(B.nbins, slack, sl, counts, start, cursor, log_n);
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_starts"))) return rc;
     tk = t_begin(h, 2, s);
@@ -486,8 +501,12 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
       else
         k_bin_wc<false><<<nw, kWcThreads, sm_wc, s>>>(h->G, B, a, b, m, per_w, vec, cursor, h->bin_ent, log_n, log_e, log_b);
     } else {           // tile counting sort (default)
-      if (prefix) k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
-      else k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent);
+      if (prefix)
+        k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent, start,
+                                                               log_n, log_e, log_b);
+      else
+        k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent, start,
+                                                                log_n, log_e, log_b);
     }
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
@@ -498,12 +517,12 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
       k_bin_apply<3, 1, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else
       k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
-    t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
-    if (h->bin_wc) {   // the scatter's overflow log (usually empty: the kernel exits at once)
+    if (h->bin_wc || sl) {   // the scatter's overflow log (usually empty: the kernel exits at once)
       k_bin_log<<<h->sms, 256, 0, s>>>(h->G, B, log_n, log_e, log_b, h->cube);
       if ((rc = launch_check(h, "k_bin_log"))) return rc;
     }
+    t_end(h, tk, s);   // the apply phase includes the overflow log
   }
   return CBAA_OK;
 }
@@ -661,7 +680,12 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
     if (h->binnable) {
-      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((2 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
+      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((3 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
+      cudaFuncSetAttribute(k_bin_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      const char* sp = std::getenv("CBAA_BIN_SAMPLE");
+      if (sp) h->bin_sample_log2 = (uint32_t)std::min(8ul, std::strtoul(sp, nullptr, 10));
+      const char* spm = std::getenv("CBAA_BIN_SAMPLE_MIN");
+      if (spm) h->bin_sample_min = std::strtoull(spm, nullptr, 10);
       cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       const char* bs = std::getenv("CBAA_BIN_SCATTER");

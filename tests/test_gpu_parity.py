@@ -598,3 +598,21 @@ def test_binned_scatter_variants(paper, scatter, monkeypatch):
     cb.update(dev(s3), dev(d3))
     ref, _ = O.update(paper, s3[:7], d3[:7])
     assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("order", ["shuffled", "sorted", "hot"])
+def test_binned_sampled_regions(paper, order, monkeypatch):
+    """Bin regions sized from a 1/16 sample (forced on small windows): whatever the sample misses spills
+    to the overflow log and still lands in the cube.  'sorted': pairs ordered by inner host, so the
+    sampled blocks see few bins and most regions overflow; 'hot': one host with 60 % of the pairs."""
+    monkeypatch.setenv("CBAA_BIN_SAMPLE_MIN", "1")
+    spec = W.WindowSpec(n=400_003, n_hosts=8000, n_flows=90_000, card_cap=400, scanners=(2000, 1300),
+                        victims=(1800,))
+    w = W.generate(spec, 51)
+    src, dst = w.src.copy(), w.dst.copy()
+    if order == "sorted":
+        o = np.argsort(src, kind="stable")
+        src, dst = src[o], dst[o]
+    elif order == "hot":
+        src[: 6 * len(src) // 10] = 0x0A000005
+    full_check(paper, src, dst, 1024, **BIN)

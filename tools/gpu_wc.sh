@@ -1,3 +1,3 @@
 set -x
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "binned" > gpurun_out/pytest_wc.log 2>&1; tail -3 gpurun_out/pytest_wc.log
-timeout 600 python tools/wc_ab.py > gpurun_out/wc_ab10.jsonl 2> gpurun_out/wc_ab10.err; cat gpurun_out/wc_ab10.jsonl; tail -3 gpurun_out/wc_ab10.err
+timeout 600 python tools/wc_ab.py > gpurun_out/wc_ab.jsonl 2> gpurun_out/wc_ab.err; cat gpurun_out/wc_ab.jsonl; tail -3 gpurun_out/wc_ab.err

@@ -1,5 +1,5 @@
-"""Binned update with the tile-sort scatter (default) vs the write-combining scatter
-(CBAA_BIN_SCATTER=wc): ms per update, per-phase ms, cube equal to the direct kernel's —
+"""Binned update variants: tile-sort scatter with exact counts (CBAA_BIN_SAMPLE=0) or sampled region sizes
+(default), write-combining scatter (CBAA_BIN_SCATTER=wc): ms per update, per-phase ms, cube equal to the direct kernel's —
     python tools/wc_ab.py > gpurun_out/wc_ab.jsonl"""
 import json
 import os
@@ -14,6 +14,8 @@ from paper_1901_06207_b200 import workload as W  # noqa: E402
 from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict  # noqa: E402
 
 PH = ["count", "starts", "scatter", "apply"]
+# tile scatter with exact counts / with sampled region sizes (default) / write-combining scatter
+VARIANTS = [("tile-exact", {"CBAA_BIN_SAMPLE": "0"}), ("tile-sampled", {}), ("wc", {"CBAA_BIN_SCATTER": "wc"})]
 
 
 def run(p, s, d, reps=10):
@@ -47,14 +49,17 @@ def main():
                   torch.randint(-2**31, 2**31 - 1, (n,), device="cuda", dtype=torch.int32, generator=g)))
     for name, s, d in cases:
         _, _, _, ref = run(dict(p, update_mode=0), s, d, reps=1)
-        for scat in ("tile", "wc"):
-            os.environ["CBAA_BIN_SCATTER"] = scat
+        for scat, env in VARIANTS:
+            for k in ("CBAA_BIN_SCATTER", "CBAA_BIN_SAMPLE"):
+                os.environ.pop(k, None)
+            os.environ.update(env)
             med, best, ph, cube = run(dict(p, update_mode=2, bin_min_pairs=1), s, d)
-            print(json.dumps({"case": name, "n": int(s.numel()), "scatter": scat, "ms_median": round(med, 4),
+            print(json.dumps({"case": name, "n": int(s.numel()), "variant": scat, "ms_median": round(med, 4),
                               "ms_best": round(best, 4), "gpairs_s": round(s.numel() / med / 1e6, 2),
                               "phases_ms": dict(zip(PH, ph)), "cube_equal_direct": bool(torch.equal(cube, ref))}),
                   flush=True)
-        os.environ.pop("CBAA_BIN_SCATTER", None)
+        for k in ("CBAA_BIN_SCATTER", "CBAA_BIN_SAMPLE"):
+            os.environ.pop(k, None)
 
 
 if __name__ == "__main__":
