@@ -476,9 +476,10 @@ def main():
         scat = "k_bin_wc" if os.environ.get("CBAA_BIN_SCATTER") == "wc" else "k_bin_scatter"
         # region sizing: a 1/16 sample (k_bin_sample) for chunks of ≥ 2^24 pairs with the tile scatter,
         # else the exact count (k_bin_count) — the library's rule (cbaa.cu update_binned)
-        samp = (scat == "k_bin_scatter" and os.environ.get("CBAA_BIN_SAMPLE", "4") != "0"
+        samp = (scat == "k_bin_scatter" and os.environ.get("CBAA_BIN_SAMPLE", "9") != "0"
                 and n >= int(os.environ.get("CBAA_BIN_SAMPLE_MIN", str(1 << 24))))
-        cnt = ("k_bin_sample", 8 * n // 16) if samp else ("k_bin_count", 8 * n)
+        lg = int(os.environ.get("CBAA_BIN_SAMPLE", "9"))
+        cnt = ("k_bin_sample", 8 * 8 * (n >> lg)) if samp else ("k_bin_count", 8 * n)
         algo = {cnt[0]: cnt[1], "k_bin_starts": 3 * 4 * 4096, scat: 12 * n,
                 "k_bin_apply": 4 * n + cb.nbytes}
         kernels = {}
@@ -491,7 +492,7 @@ def main():
         kd = kernels[dom]
         roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
                     "frac": kd["frac_hbm"], "traffic": kd["ncu_dram_bytes"],
-                    "algorithmic": {cnt[0]: "8 B/pair read" + (" for 1/16 of the pairs" if samp else ""),
+                    "algorithmic": {cnt[0]: "8 B/pair read" + (f" for 8 of every {1 << lg} pairs" if samp else ""),
                                     scat: "8 B/pair read + 4 B/pair entry written",
                                     "k_bin_apply": "4 B/pair entry read + the cube's words OR-ed once (+ overflow "
                                                    "log, normally empty)"},

@@ -131,11 +131,14 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_count(const __grid_consta
   }
 }
 
-// Phase 1, sampled (default for large normalised windows): the histogram of every 2^L-th block of
-// kSampleBlk pairs only (1/16 of the input); k_bin_starts scales it up with a safety margin.  A region
-// that still turns out too small spills its excess entries to the overflow log (k_bin_log), so the cube
-// is exact for any input — the sample only decides how much of the work takes the fast path.
-constexpr uint32_t kSampleBlk = 4u * kCountThreads;   // 4096 pairs, one 16-B quad per thread
+// Phase 1, sampled (default for large normalised windows): the histogram of 8 consecutive pairs — one
+// 32-B sector of each array — out of every 2^L pairs (L = 9: 1/64 of the pairs and of the input's DRAM
+// sectors); k_bin_starts scales it up with a margin.  Units of 8 pairs, not large blocks, so a flow
+// whose packets arrive in one burst is sampled in proportion to its length instead of all-or-nothing.
+// A region that still turns out too small spills its excess entries to the overflow log (k_bin_log), so
+// the cube is exact for any input — the sample only decides how much of the work takes the fast path.
+constexpr uint32_t kSampleUnit = 8;                // pairs per sample unit (one sector per array)
+constexpr int kSampleUnroll = 2;
 __global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
                                                             const uint32_t* __restrict__ src,
                                                             const uint32_t* __restrict__ dst, uint64_t n,
@@ -143,17 +146,36 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_const
   extern __shared__ uint32_t hist[];
   for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads) hist[b] = 0;
   __syncthreads();
-  const uint64_t nblk = (n + kSampleBlk - 1) / kSampleBlk;
-  for (uint64_t sb = blockIdx.x; (sb << stride_log2) < nblk; sb += gridDim.x) {
-    const uint64_t k0 = (sb << stride_log2) * kSampleBlk, c1 = min(n, k0 + kSampleBlk);
-    uint32_t ss[4], dd[4];
-    bool in[4];
-    load_quad(src, dst, k0 + 4ull * threadIdx.x, c1, vec, ss, dd, in);
+  const uint64_t nu = (n + (1ull << stride_log2) - 1) >> stride_log2;   // units: pairs [u·2^L, u·2^L + 8)
+  const uint64_t step = (uint64_t)gridDim.x * kCountThreads;
+  for (uint64_t u0 = (uint64_t)blockIdx.x * kCountThreads + threadIdx.x; u0 < nu; u0 += step * kSampleUnroll) {
+    uint32_t ss[kSampleUnroll][kSampleUnit], dd[kSampleUnroll][kSampleUnit];
+    uint32_t cnt[kSampleUnroll];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t bin, ent;
-      if (in[e] && pair_bin<false>(G, B, ss[e], dd[e], bin, ent)) atomicAdd(&hist[bin], 1u);
+    for (int v = 0; v < kSampleUnroll; ++v) {
+      const uint64_t k = (u0 + v * step) << stride_log2;
+      cnt[v] = u0 + v * step < nu ? (n - k >= kSampleUnit ? kSampleUnit : (uint32_t)(n - k)) : 0u;
+      if (vec && cnt[v] == kSampleUnit) {
+        const uint4 a0 = ld_stream4(src + k), a1 = ld_stream4(src + k + 4), b0 = ld_stream4(dst + k), b1 = ld_stream4(dst + k + 4);
+        ss[v][0] = a0.x, ss[v][1] = a0.y, ss[v][2] = a0.z, ss[v][3] = a0.w;
+        ss[v][4] = a1.x, ss[v][5] = a1.y, ss[v][6] = a1.z, ss[v][7] = a1.w;
+        dd[v][0] = b0.x, dd[v][1] = b0.y, dd[v][2] = b0.z, dd[v][3] = b0.w;
+        dd[v][4] = b1.x, dd[v][5] = b1.y, dd[v][6] = b1.z, dd[v][7] = b1.w;
+      } else {
+#pragma unroll
+        for (uint32_t e = 0; e < kSampleUnit; ++e) {
+          ss[v][e] = e < cnt[v] ? __ldcs(src + k + e) : 0u;
+          dd[v][e] = e < cnt[v] ? __ldcs(dst + k + e) : 0u;
+        }
+      }
     }
+#pragma unroll
+    for (int v = 0; v < kSampleUnroll; ++v)
+#pragma unroll
+      for (uint32_t e = 0; e < kSampleUnit; ++e) {
+        uint32_t bin, ent;
+        if (e < cnt[v] && pair_bin<false>(G, B, ss[v][e], dd[v][e], bin, ent)) atomicAdd(&hist[bin], 1u);
+      }
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < B.nbins; b += kCountThreads)
@@ -162,14 +184,17 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_const
 
 // Phase 2: bin regions.  start[b] = Σ_{b' < b} cap(b') with cap(b) = align8(counts[b] + slack) for exact
 // counts (sector-aligned; slack = the duplicate padding k_bin_wc may add, 8 entries per CTA), or, for a
-// 1/2^L sample, the scaled count est = counts[b]·2^L plus est/4 + 64; start[nbins] = total, cursor :=
+// sample of 8 pairs per 2^L, the scaled count est = counts[b]·2^L/8 plus est/4 + 2·sqrt(2^L·est) + 64; start[nbins] = total, cursor :=
 // start (the scatter's bump allocator; the apply reads [start[b], min(cursor[b], start[b + 1]))),
 // counts := 0 for the next round, the overflow-log count := 0.  One CTA (nbins ≤ 16384).
 constexpr int kStartThreads = 1024;
 __device__ __forceinline__ uint32_t bin_cap(uint32_t c, uint32_t slack, uint32_t sample_log2) {
   if (!sample_log2) return (c + slack + 7u) & ~7u;
-  const uint32_t est = c << sample_log2;
-  return (est + est / 4u + 64u + slack + 7u) & ~7u;
+  // est = c·2^L/8; sampled in units of 8 pairs, its error is at most ~sqrt(2^L·est) (a bin's pairs
+  // clustered in whole units): margin est/4 + 2·sqrt(2^L·est) + 64
+  const uint32_t est = (c << sample_log2) / kSampleUnit;
+  const uint32_t sd = (uint32_t)sqrtf((float)est * (float)(1u << sample_log2));
+  return (est + est / 4u + 2u * sd + 64u + slack + 7u) & ~7u;
 }
 __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, uint32_t slack, uint32_t sample_log2,
                                                               uint32_t* __restrict__ counts,

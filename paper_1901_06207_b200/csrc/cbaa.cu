@@ -82,7 +82,7 @@ struct cbaa_handle {
   uint32_t* bin_tab = nullptr;    // counts | start | cursor | log count
   void* bin_log = nullptr;        // k_bin_wc overflow log
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
-  uint32_t bin_sample_log2 = 4;   // regions sized from a 1/2^L sample (0: exact count; CBAA_BIN_SAMPLE)
+  uint32_t bin_sample_log2 = 9;   // regions sized from 8 pairs of every 2^L (0: exact count; CBAA_BIN_SAMPLE)
   uint64_t bin_sample_min = 1ull << 24;   // chunks with fewer pairs are counted exactly (CBAA_BIN_SAMPLE_MIN)
   // per-kernel update timing (cbaa_set_phase_timing)
   int timing = 0;
@@ -433,17 +433,20 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   const uint64_t kChunk = h->bin_chunk;
   const BinGeo& B = h->B;
   // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
-  const uint32_t slack = 8u * (uint32_t)h->sms;
+  const uint32_t slack = h->bin_wc ? 8u * (uint32_t)h->sms : 0u;
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
   // sampled region sizing (k_bin_sample): normalised input, tile scatter, chunks of ≥ bin_sample_min pairs
   const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
   const uint64_t mx = std::min(n, kChunk);
   const bool any_sampled = samp && mx >= h->bin_sample_min;
-  // Σ cap(b) ≤ exact: m + nbins·(slack + 7); sampled: 1.25·(m + 2^L·4096) + nbins·(64 + slack + 7)
-  const uint64_t want = std::max<uint64_t>(mx + (uint64_t)(slack + 8) * B.nbins,
-                                           any_sampled ? (mx + ((uint64_t)kSampleBlk << samp)) * 5 / 4 +
-                                                             (uint64_t)(slack + 72) * B.nbins
-                                                       : 0);
+  // Σ cap(b) ≤ exact: m + nbins·(slack + 7); sampled (Σ est ≤ m + 2^L, Cauchy-Schwarz on the √ terms):
+  // 1.25·(m + 2^L) + 2·√(nbins·2^L·(m + 2^L)) + nbins·(64 + slack + 7)
+  const double sm_ = (double)(mx + (1ull << samp));
+  const uint64_t want = std::max<uint64_t>(
+      mx + (uint64_t)(slack + 8) * B.nbins,
+      any_sampled ? (uint64_t)(1.25 * sm_ + 2.0 * std::sqrt((double)B.nbins * (double)(1ull << samp) * sm_)) +
+                        (uint64_t)(slack + 72) * B.nbins + 64
+                  : 0);
   if (h->bin_cap < want) {
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
     h->bin_ent = nullptr;
@@ -683,7 +686,10 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((3 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
       cudaFuncSetAttribute(k_bin_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       const char* sp = std::getenv("CBAA_BIN_SAMPLE");
-      if (sp) h->bin_sample_log2 = (uint32_t)std::min(8ul, std::strtoul(sp, nullptr, 10));
+      if (sp) {
+        const unsigned long v = std::strtoul(sp, nullptr, 10);
+        h->bin_sample_log2 = v == 0 ? 0u : (uint32_t)std::min(16ul, std::max(3ul, v));
+      }
       const char* spm = std::getenv("CBAA_BIN_SAMPLE_MIN");
       if (spm) h->bin_sample_min = std::strtoull(spm, nullptr, 10);
       cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);

@@ -600,14 +600,17 @@ def test_binned_scatter_variants(paper, scatter, monkeypatch):
     assert np.array_equal(gpu_cube(cb), ref)
 
 
-@pytest.mark.parametrize("order", ["shuffled", "sorted", "hot"])
-def test_binned_sampled_regions(paper, order, monkeypatch):
-    """Bin regions sized from a 1/16 sample (forced on small windows): whatever the sample misses spills
-    to the overflow log and still lands in the cube.  'sorted': pairs ordered by inner host, so the
-    sampled blocks see few bins and most regions overflow; 'hot': one host with 60 % of the pairs."""
+@pytest.mark.parametrize("order, sample", [("shuffled", "9"), ("sorted", "9"), ("hot", "9"), ("shuffled", "14"),
+                                           ("bursty", "14"), ("bursty", "3")])
+def test_binned_sampled_regions(paper, order, sample, monkeypatch):
+    """Bin regions sized from 8 of every 2^L pairs (forced on small windows): whatever the sample misses
+    spills to the overflow log and still lands in the cube.  'sorted': pairs ordered by inner host;
+    'hot': one host with 60 % of the pairs; L = 14 leaves most bins unsampled, so most regions
+    overflow; 'bursty': each flow's packets contiguous; L = 3: every pair sampled."""
     monkeypatch.setenv("CBAA_BIN_SAMPLE_MIN", "1")
+    monkeypatch.setenv("CBAA_BIN_SAMPLE", sample)
     spec = W.WindowSpec(n=400_003, n_hosts=8000, n_flows=90_000, card_cap=400, scanners=(2000, 1300),
-                        victims=(1800,))
+                        victims=(1800,), order="bursty" if order == "bursty" else "shuffled")
     w = W.generate(spec, 51)
     src, dst = w.src.copy(), w.dst.copy()
     if order == "sorted":

@@ -41,8 +41,13 @@ def run(p, s, d, reps=10):
 def main():
     p = O.default_params()
     cases = []
-    w = W.generate(W.C2, 1, with_raw=False)
-    cases.append(("C2", torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda()))
+    import dataclasses
+    for name, spec in (("C2", W.C2), ("C2 bursty", dataclasses.replace(W.C2, order="bursty"))):
+        if len(sys.argv) > 1 and name not in sys.argv[1:]:
+            continue
+        w = W.generate(spec, 1, with_raw=False)
+        cases.append((name, torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda()))
+        del w
     g = torch.Generator(device="cuda").manual_seed(5)
     n = 100_000_000
     cases.append(("uniform", torch.randint(-2**31, 2**31 - 1, (n,), device="cuda", dtype=torch.int32, generator=g),
