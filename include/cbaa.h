@@ -165,10 +165,16 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
  * update_mode the word is loaded first and only a missing bit is ORed in — the
  * cube is identical either way.  With CBAA_UPDATE_BINNED and n above the
  * handle's threshold the pairs are first binned by (CS, row group) into a
- * device scratch of 4 B per pair (≤ 2^28 pairs per chunk, allocated on first
- * use) and the bits are set in shared memory, then OR-ed into the cube; below
- * the threshold, or for geometries whose tables do not fit, the call takes the
- * test-and-set kernel.  Updates accumulate until cbaa_reset; calls on
+ * device scratch of ~4-6 B per pair plus a 6 B/pair overflow log (≤ 2^28 pairs
+ * per chunk, allocated on first use) and the bits are set in shared memory,
+ * then OR-ed into the cube; below the threshold, or for geometries whose
+ * tables do not fit, the call takes the test-and-set kernel.  Chunks of
+ * ≥ 2^24 normalised pairs size their bin regions from a sample (8 of every
+ * 512 pairs); entries that overflow a region are applied from the overflow
+ * log, so the cube never depends on the sample.  Environment knobs read at
+ * cbaa_create (tests, A/B): CBAA_BIN_SAMPLE (log2 of the sampling period,
+ * 0 = exact count), CBAA_BIN_SAMPLE_MIN, CBAA_BIN_SCATTER=wc (write-combining
+ * scatter, exact count), CBAA_BIN_CHUNK, CBAA_BIN_MIN.  Updates accumulate until cbaa_reset; calls on
  * one handle must be stream-ordered with its detect/merge/reset.  Any 4-byte
  * alignment is accepted (16-B aligned arrays take the vector path).  Async on
  * stream. */
@@ -302,8 +308,8 @@ uint32_t cbaa_update_passes(const cbaa_handle* h);
  * the stream that kernel is launched on.  cbaa_update_phase_ms synchronizes
  * those events and writes the milliseconds summed per phase over all update
  * calls since the previous query (or since enabling) into ms[0..3]:
- *   binned path: ms[0] k_bin_count, ms[1] k_bin_starts, ms[2] k_bin_scatter,
- *                ms[3] k_bin_apply;
+ *   binned path: ms[0] k_bin_sample or k_bin_count, ms[1] k_bin_starts,
+ *                ms[2] k_bin_scatter (or k_bin_wc), ms[3] k_bin_apply + k_bin_log;
  *   direct path: ms[0] k_update (every pass), ms[1..3] = 0,
  * and the number of update calls in *calls (nullable).  ms needs cap >= 4
  * (CBAA_E_ARG otherwise).  Host-side bookkeeping only; kernels are unchanged. */
