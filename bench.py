@@ -500,7 +500,11 @@ def main():
                     "stream over the timed region (cbaa_set_phase_timing), averaged per update call",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernels": kernels,
                     "update_ms": upd, "update_mode": args.update_mode,
-                    "traffic_source": "profiles/r01_ncu_binned.json (ncu --set full, dram__bytes_read+write)"}
+                    "traffic_source": "profiles/r01_ncu_binned.json (ncu --set full, dram__bytes_read+write)",
+                    "limiter": "the dominant binned kernel is not DRAM-bound (ncu DRAM traffic = its algorithmic "
+                                "bytes): k_bin_scatter is issue/latency-bound (ATOMS rank, per-tile bin scan, "
+                                "4 barriers per 8192-pair tile, 16 warps/SM at 119 registers), k_bin_apply is "
+                                "shared-memory-bound (4 random LDS tests per entry); see DESIGN.md section 6"}
         roofline_hbm = None
     else:
         algo = 4 * n                       # |RA|+|VA| = 4 bit-sets per pair, one random word each
