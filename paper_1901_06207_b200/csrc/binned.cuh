@@ -560,6 +560,12 @@ __device__ __forceinline__ uint32_t lds(uint32_t a) {
 __device__ __forceinline__ void reds_or(uint32_t a, uint32_t bit) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit));
 }
+// RED.OR of `bit` unless the loaded word v already has it, as one predicated instruction (a C++ `if`
+// around the asm costs a BSSY/BRA/BSYNC triple per array and entry)
+__device__ __forceinline__ void reds_or_if_clear(uint32_t a, uint32_t bit, uint32_t v) {
+  asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %2, 0;\n @p red.shared.or.b32 [%0], %1;\n}" ::"r"(a), "r"(bit),
+               "r"(v & bit));
+}
 
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the
 // group (word i = word w of column i of CS cs, columns of all arrays in S:116 order), which is then
@@ -632,8 +638,7 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
         v[a] = lds(adr[a]);
       }
 #pragma unroll
-      for (int a = 0; a < NRA + NVA; ++a)
-        if (!(v[a] & bit)) reds_or(adr[a], bit);
+      for (int a = 0; a < NRA + NVA; ++a) reds_or_if_clear(adr[a], bit, v[a]);
     } else {
       for (uint32_t a = 0; a < narr; ++a) {
         const uint32_t adr = sbase + 4u * ((G.arr_off[a] >> G.wpc_log2) + lp_col(G, dbl, lp, a));
