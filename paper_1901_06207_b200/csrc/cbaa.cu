@@ -440,12 +440,12 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
   const uint64_t mx = std::min(n, kChunk);
   const bool any_sampled = samp && mx >= h->bin_sample_min;
   // Σ cap(b) ≤ exact: m + nbins·(slack + 7); sampled (Σ est ≤ m + 2^L, Cauchy-Schwarz on the √ terms):
-  // 1.25·(m + 2^L) + 2·√(nbins·2^L·(m + 2^L)) + nbins·(64 + slack + 7)
+  // 1.25·(m + 2^L) + 2·√(nbins·2^L·(m + 2^L)) + nbins·(64 + slack + 7 + 2 for sqrtf rounding)
   const double sm_ = (double)(mx + (1ull << samp));
   const uint64_t want = std::max<uint64_t>(
       mx + (uint64_t)(slack + 8) * B.nbins,
       any_sampled ? (uint64_t)(1.25 * sm_ + 2.0 * std::sqrt((double)B.nbins * (double)(1ull << samp) * sm_)) +
-                        (uint64_t)(slack + 72) * B.nbins + 64
+                        (uint64_t)(slack + 80) * B.nbins + 64   // + 7 alignment, + sqrtf rounding per bin
                   : 0);
   if (h->bin_cap < want) {
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
