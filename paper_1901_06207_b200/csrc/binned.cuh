@@ -609,23 +609,8 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
     }
     if constexpr (NVA == 1) vseed = pin(G.va_seeds[0]);
   }
-  // kb ≤ 2 (r ≥ 4, the paper's geometry): the valid entries of the group's bins are walked as one
-  // virtual range [0, len0 + len1) — bin 0's then bin 1's — so no padding or spare capacity is read;
-  // kb > 2: positions [P0, P1) with a per-entry bin search and validity check
-  const uint32_t len0 = E0 - P0, len1 = kb == 2 ? E1 - B1 : 0u;
-  const uint32_t V = kb <= 2 ? len0 + len1 : P1 - P0;
-  auto at = [&](uint32_t v) -> uint32_t { return kb <= 2 ? (v < len0 ? P0 + v : B1 + (v - len0)) : P0 + v; };
-  auto apply_one = [&](uint32_t e, uint32_t v) {
-    uint32_t hi = 0;
-    if (kb == 2) {
-      hi = v >= len0 ? 1u << es : 0u;
-    } else if (kb > 2) {
-      const uint32_t q = P0 + v;
-      uint32_t k = 0;
-      for (uint32_t j = 1; j < kb; ++j) k += q >= start[b0 + j] ? 1u : 0u;
-      if (q >= min(end[(b0 + k) * kCurStride], start[b0 + k + 1])) return;
-      hi = k << es;
-    }
+  // the entry's |RA|+|VA| bits, row bit `hi | (e mod 2^s)`, set in the shared image (test first)
+  auto set_bits = [&](uint32_t e, uint32_t hi) {
     const uint32_t lp = e >> es, bit = 1u << (hi | (e & smask));
     const uint64_t dbl = ((uint64_t)lp << L) | lp;
     if constexpr (NRA > 0) {
@@ -646,28 +631,49 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
       }
     }
   };
-  constexpr uint32_t kStep = kApplyUnroll * kApplyThreads;
-  uint32_t e[kApplyUnroll];
-  uint32_t p = threadIdx.x;
+  // kb > 2: position q of [P0, P1) → its bin by search, skipped if past that bin's valid end
+  auto set_bits_at = [&](uint32_t e, uint32_t v) {
+    const uint32_t q = P0 + v;
+    uint32_t k = 0;
+    for (uint32_t j = 1; j < kb; ++j) k += q >= start[b0 + j] ? 1u : 0u;
+    if (q >= min(end[(b0 + k) * kCurStride], start[b0 + k + 1])) return;
+    set_bits(e, k << es);
+  };
+  // one contiguous range of entries, kApplyUnroll per thread in flight (the next batch's loads are
+  // issued before the current batch is applied)
+  auto walk = [&](const uint32_t* __restrict__ ent, uint32_t len, uint32_t hi, bool search) {
+    constexpr uint32_t kStep = kApplyUnroll * kApplyThreads;
+    uint32_t e[kApplyUnroll];
+    uint32_t p = threadIdx.x;
 #pragma unroll
-  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kApplyThreads < V ? __ldcs(entries + at(p + u * kApplyThreads)) : 0u;
-  while (p < V) {
-    const uint32_t pn = p + kStep;
-    uint32_t en[kApplyUnroll];
-#pragma unroll
-    for (int u = 0; u < kApplyUnroll; ++u)
-      en[u] = pn + u * kApplyThreads < V ? __ldcs(entries + at(pn + u * kApplyThreads)) : 0u;
-    if (p + (kApplyUnroll - 1) * kApplyThreads < V) {   // whole batch: no per-entry bound checks
-#pragma unroll
-      for (int u = 0; u < kApplyUnroll; ++u) apply_one(e[u], p + u * kApplyThreads);
-    } else {
+    for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kApplyThreads < len ? __ldcs(ent + p + u * kApplyThreads) : 0u;
+    while (p < len) {
+      const uint32_t pn = p + kStep;
+      uint32_t en[kApplyUnroll];
 #pragma unroll
       for (int u = 0; u < kApplyUnroll; ++u)
-        if (p + u * kApplyThreads < V) apply_one(e[u], p + u * kApplyThreads);
-    }
+        en[u] = pn + u * kApplyThreads < len ? __ldcs(ent + pn + u * kApplyThreads) : 0u;
+      if (p + (kApplyUnroll - 1) * kApplyThreads < len) {   // whole batch: no per-entry bound checks
 #pragma unroll
-    for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
-    p = pn;
+        for (int u = 0; u < kApplyUnroll; ++u) search ? set_bits_at(e[u], p + u * kApplyThreads) : set_bits(e[u], hi);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kApplyUnroll; ++u)
+          if (p + u * kApplyThreads < len) search ? set_bits_at(e[u], p + u * kApplyThreads) : set_bits(e[u], hi);
+      }
+#pragma unroll
+      for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
+      p = pn;
+    }
+  };
+  // kb ≤ 2 (r ≥ 4, the paper's geometry): each bin's valid entries [start, min(cursor, next start)) as its
+  // own range with a constant row bit, so no padding or spare capacity is read and no entry needs a bin
+  // lookup; kb > 2: positions [P0, P1) with the per-entry search
+  if (kb <= 2) {
+    walk(entries + P0, E0 - P0, 0u, false);
+    if (kb == 2) walk(entries + B1, E1 - B1, 1u << es, false);
+  } else {
+    walk(entries + P0, P1 - P0, 0u, true);
   }
   __syncthreads();
   uint32_t* cw = cube + (uint64_t)cs * G.cs_words + w;
