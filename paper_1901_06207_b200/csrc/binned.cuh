@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
 // Phase 3 (default): entries of CTA j's chunk, tile by tile: rank within the tile by ATOMS on
 // the tile's bin counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
 // shared-memory counting sort, then the runs written out.
-template <bool PREFIX>
+template <bool PREFIX, int NB>   // NB: the bin count at compile time (4096: paper geometry), 0: run time
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ src,
@@ -255,10 +255,11 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
   __shared__ uint32_t s_w[kBinThreads / 32];
   __shared__ int s_ovf;                                  // some run of this tile passes its region's end
   const uint32_t tid = threadIdx.x;
-  for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
+  const uint32_t nbins = NB ? (uint32_t)NB : B.nbins;
+  for (uint32_t b = tid; b < nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
   if (tid == 0) s_ovf = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
-  const uint32_t wchunk = (B.nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
+  const uint32_t wchunk = (nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
   const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), pgm = pin(G.g - 1u);
   const uint32_t prm = pin(G.rmask), pr = pin(G.r), pbl = pin(B.bpc_log2), pes = pin(B.s);
   const uint32_t psm = pin((1u << B.s) - 1u), toff_sa = pin(smem_addr(toff));
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const uint32_t b = w0 + i0 + 32 * j + lane;
-          x[j] = (i0 + 32 * j < wchunk && b < B.nbins) ? toff[b] : 0u;
+          x[j] = (i0 + 32 * j < wchunk && b < nbins) ? toff[b] : 0u;
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + (w0 + i0 + 32 * j + lane) * kCurStride, x[j]) : 0u;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const uint32_t b = w0 + i0 + 32 * j + lane;
-          if (i0 + 32 * j < wchunk && b < B.nbins) {
+          if (i0 + 32 * j < wchunk && b < nbins) {
             const uint32_t x = toff[b];
             toff[b] = run;
             if (x) base[b] -= run;   // base[b] + p is the slot of staging position p
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
           }
         }
       }
-      if (tid == 0) toff[B.nbins] = tot;
+      if (tid == 0) toff[nbins] = tot;
     }
     __syncthreads();
 #pragma unroll
@@ -365,8 +366,9 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
       sbin[pos] = (uint16_t)bin;
     }
     __syncthreads();
-    const uint32_t total = toff[B.nbins];
+    const uint32_t total = toff[nbins];
     if (!s_ovf) {
+#pragma unroll 4
       for (uint32_t p = tid; p < total; p += kBinThreads) entries[base[sbin[p]] + p] = stage[p];
     } else {   // entries past their region's end (a sampled capacity fell short) go to the overflow log
       for (uint32_t p = tid; p < total; p += kBinThreads) {
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
       }
     }
     __syncthreads();
-    for (uint32_t b = tid; b < B.nbins; b += kBinThreads) toff[b] = 0;
+    for (uint32_t b = tid; b < nbins; b += kBinThreads) toff[b] = 0;
     if (tid == 0) s_ovf = 0;
     __syncthreads();
   }

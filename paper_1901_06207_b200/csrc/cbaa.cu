@@ -505,11 +505,14 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
         k_bin_wc<false><<<nw, kWcThreads, sm_wc, s>>>(h->G, B, a, b, m, per_w, vec, cursor, h->bin_ent, log_n, log_e, log_b);
     } else {           // tile counting sort (default)
       if (prefix)
-        k_bin_scatter<true><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent, start,
-                                                               log_n, log_e, log_b);
+        k_bin_scatter<true, 0><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
+                                                                  start, log_n, log_e, log_b);
+      else if (B.nbins == 4096)   // the paper geometry: bin loops with compile-time trip counts
+        k_bin_scatter<false, 4096><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
+                                                                      start, log_n, log_e, log_b);
       else
-        k_bin_scatter<false><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent, start,
-                                                                log_n, log_e, log_b);
+        k_bin_scatter<false, 0><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
+                                                                   start, log_n, log_e, log_b);
     }
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
@@ -699,10 +702,12 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       const int sm_wc = (int)wc_smem_bytes(B.nbins);
       cudaFuncSetAttribute(k_bin_wc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
       cudaFuncSetAttribute(k_bin_wc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
-      cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_apply<3, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
       cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
       cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
