@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kStartThreads) k_bin_starts(uint32_t nbins, ui
 // Phase 3 (default): entries of CTA j's chunk, tile by tile: rank within the tile by ATOMS on
 // the tile's bin counts, a block scan of those counts (which also reserves each run at its bin's global cursor), a
 // shared-memory counting sort, then the runs written out.
-template <bool PREFIX, int NB>   // NB: the bin count at compile time (4096: paper geometry), 0: run time
+template <bool PREFIX, int NB>   // NB: the bin count at compile time (4096; −1: the paper geometry), 0: run time
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ src,
@@ -255,14 +255,19 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
   __shared__ uint32_t s_w[kBinThreads / 32];
   __shared__ int s_ovf;                                  // some run of this tile passes its region's end
   const uint32_t tid = threadIdx.x;
-  const uint32_t nbins = NB ? (uint32_t)NB : B.nbins;
+  const uint32_t nbins = NB < 0 ? 4096u : NB ? (uint32_t)NB : B.nbins;
   for (uint32_t b = tid; b < nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
   if (tid == 0) s_ovf = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t wchunk = (nbins + kBinThreads - 1) / kBinThreads * 32;   // bins per warp (multiple of 32)
-  const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), pgm = pin(G.g - 1u);
-  const uint32_t prm = pin(G.rmask), pr = pin(G.r), pbl = pin(B.bpc_log2), pes = pin(B.s);
-  const uint32_t psm = pin((1u << B.s) - 1u), toff_sa = pin(smem_addr(toff));
+  const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed);
+  // NB < 0: the paper geometry (r = 4, g = 4096, s = 4, 256 bins per CS) with its shifts and masks as
+  // immediates; otherwise pinned in registers
+  constexpr bool kPaper = NB < 0;
+  const uint32_t pgm = kPaper ? 4095u : pin(G.g - 1u);
+  const uint32_t prm = kPaper ? 15u : pin(G.rmask), pr = kPaper ? 4u : pin(G.r);
+  const uint32_t pbl = kPaper ? 8u : pin(B.bpc_log2), pes = kPaper ? 4u : pin(B.s);
+  const uint32_t psm = kPaper ? 15u : pin((1u << B.s) - 1u), toff_sa = pin(smem_addr(toff));
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
     // all kBinPPT pairs of the thread are loaded before any is hashed (one DRAM latency per tile), then

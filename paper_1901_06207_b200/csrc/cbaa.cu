@@ -507,7 +507,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
       if (prefix)
         k_bin_scatter<true, 0><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
                                                                   start, log_n, log_e, log_b);
-      else if (B.nbins == 4096)   // the paper geometry: bin loops with compile-time trip counts
+      else if (B.nbins == 4096 && h->G.r == 4 && h->G.g == 4096)   // the paper geometry: constants inlined
+        k_bin_scatter<false, -1><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
+                                                                    start, log_n, log_e, log_b);
+      else if (B.nbins == 4096)   // bin loops with compile-time trip counts
         k_bin_scatter<false, 4096><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
                                                                       start, log_n, log_e, log_b);
       else
@@ -704,6 +707,8 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       cudaFuncSetAttribute(k_bin_wc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
       cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      cudaFuncSetAttribute(k_bin_scatter<false, -1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
       cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
