@@ -577,7 +577,9 @@ __device__ __forceinline__ void reds_or_if_clear(uint32_t a, uint32_t bit, uint3
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the
 // group (word i = word w of column i of CS cs, columns of all arrays in S:116 order), which is then
 // OR-ed into the cube.  The CTA owns those words for the whole launch.  <3, 1>: paper shape unrolled.
-template <int NRA, int NVA, int S>
+// P: the paper's default configuration (3 RAs + 1 VA of 4096 columns, clbs [0, 10, 20], cbn 12, r = 4):
+// extraction shifts, masks and array offsets in the image as immediates
+template <int NRA, int NVA, int S, bool P = false>
 __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_constant__ Geo G,
                                                              const __grid_constant__ BinGeo B,
                                                              const uint32_t* __restrict__ start,
@@ -624,9 +626,12 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
       uint32_t adr[NRA + NVA], v[NRA + NVA];
 #pragma unroll
       for (int a = 0; a < NRA + NVA; ++a) {
-        const uint32_t col = a < NRA ? (uint32_t)(dbl >> shv[a < NRA ? a : 0]) & mk[a]
-                                     : mix32(lp ^ (NVA == 1 ? vseed : G.va_seeds[a - NRA])) & mk[a];
-        adr[a] = ab[a] + 4u * col;
+        constexpr uint32_t kSh[3] = {44u, 34u, 24u};   // 2L − clbs(i) − cbn(i) at the paper configuration
+        const uint32_t sh_a = P ? kSh[a < 3 ? a : 0] : shv[a < NRA ? a : 0];
+        const uint32_t mk_a = P ? 4095u : mk[a];
+        const uint32_t col = a < NRA ? (uint32_t)(dbl >> sh_a) & mk_a
+                                     : mix32(lp ^ (NVA == 1 ? vseed : G.va_seeds[a - NRA])) & mk_a;
+        adr[a] = (P ? sbase + 16384u * (uint32_t)a : ab[a]) + 4u * col;
         v[a] = lds(adr[a]);
       }
 #pragma unroll

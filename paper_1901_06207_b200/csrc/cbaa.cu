@@ -82,6 +82,7 @@ struct cbaa_handle {
   uint32_t* bin_tab = nullptr;    // counts | start | cursor | log count
   void* bin_log = nullptr;        // k_bin_wc overflow log
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
+  bool apply_paper = false;       // k_bin_apply<3, 1, 4, true>: the paper's default configuration
   uint32_t bin_sample_log2 = 9;   // regions sized from 8 pairs of every 2^L (0: exact count; CBAA_BIN_SAMPLE)
   uint64_t bin_sample_min = 1ull << 24;   // chunks with fewer pairs are counted exactly (CBAA_BIN_SAMPLE_MIN)
   // per-kernel update timing (cbaa_set_phase_timing)
@@ -520,7 +521,9 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
     tk = t_begin(h, 3, s);
-    if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
+    if (h->apply_paper)
+      k_bin_apply<3, 1, 4, true><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
+    else if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
       k_bin_apply<3, 1, 4><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else if (h->G.num_ra == 3 && h->G.num_va == 1)
       k_bin_apply<3, 1, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
@@ -714,6 +717,13 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_apply<3, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      cudaFuncSetAttribute(k_bin_apply<3, 1, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      {   // the paper's default configuration: k_bin_apply<3, 1, 4, true> with constants inlined
+        const Geo& g = h->G;
+        bool pp = g.num_ra == 3 && g.num_va == 1 && B.s == 4 && g.sh[0] == 44 && g.sh[1] == 34 && g.sh[2] == 24;
+        for (uint32_t a = 0; a < 4 && pp; ++a) pp = g.colmask[a] == 4095u && (g.arr_off[a] >> g.wpc_log2) == 4096u * a;
+        h->apply_paper = pp;
+      }
       cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
       cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
     }
