@@ -619,3 +619,20 @@ def test_binned_sampled_regions(paper, order, sample, monkeypatch):
     elif order == "hot":
         src[: 6 * len(src) // 10] = 0x0A000005
     full_check(paper, src, dst, 1024, **BIN)
+
+
+@pytest.mark.parametrize("off_s, off_d", [(1, 1), (0, 3)])
+def test_binned_sampled_misaligned(paper, off_s, off_d, monkeypatch):
+    """Sampled regions on arrays that are not 16-B aligned (the sample's scalar loads, the scatter's
+    per-pair path) and differently aligned src/dst."""
+    monkeypatch.setenv("CBAA_BIN_SAMPLE_MIN", "1")
+    src, dst = W.random_pairs(300_000, 17)
+    big_s = dev(np.concatenate([np.zeros(4, np.uint32), src]))
+    big_d = dev(np.concatenate([np.zeros(4, np.uint32), dst]))
+    n = 290_001
+    cb = handle(paper, **BIN)
+    cb.reset()
+    cb.update(big_s[off_s: off_s + n], big_d[off_d: off_d + n])
+    ref, _ = O.update(paper, big_s.cpu().numpy().view(np.uint32)[off_s: off_s + n],
+                      big_d.cpu().numpy().view(np.uint32)[off_d: off_d + n])
+    assert np.array_equal(gpu_cube(cb), ref)
