@@ -72,7 +72,8 @@ typedef struct cbaa_handle cbaa_handle;
  * cbaa_config_validate: 1 ≤ r ≤ 16 (or 0); 2 ≤ num_ra ≤ 8; num_va ≤ 8;
  * g a power of two ≥ 32 (Q28); mangle_a odd; 1 ≤ cbn(i) ≤ min(32−r, 24);
  * clbs strictly increasing and < L = 32−r (Q6); Σ|EP(i)| = L; 0 ≤ |CP(i)| ≤
- * |EP((i+1) mod num_ra)|; cube ≤ 16 GiB. */
+ * |EP((i+1) mod num_ra)|; cube ≤ 16 GiB; bytes per CS (Σ c(i)·g/8) a multiple
+ * of 16 (GPU word layout: only g = 32 with a 2-column array can miss it). */
 typedef struct {
   uint32_t r;                          /* right bits of the mangled inner IP selecting the CS */
   uint32_t num_ra, num_va;             /* |RA|, |VA|                                            */

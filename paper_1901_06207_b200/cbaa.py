@@ -259,20 +259,25 @@ class Cbaa:
     def update_host(self, src, dst, stream=None):
         """Alg. 1 over HOST arrays (numpy or CPU tensors, ideally pinned): pipelined H2D inside the library."""
         import torch
-        ps, pd = [], []
-        for a, lst in ((src, ps), (dst, pd)):
+        keep, ptrs = [], []   # converted copies stay referenced until the library call returns
+        for a in (src, dst):
             if isinstance(a, torch.Tensor):
-                if a.is_cuda or not a.is_contiguous() or a.element_size() != 4:
-                    raise TypeError("update_host needs contiguous 32-bit CPU tensors")
-                lst.append(a.data_ptr())
+                if a.is_cuda or not a.is_contiguous() or a.dtype not in (torch.int32, torch.uint32):
+                    raise TypeError("update_host needs contiguous int32/uint32 CPU tensors")
+                keep.append(a)
+                ptrs.append(a.data_ptr())
             else:
                 a = np.ascontiguousarray(a)
-                if a.dtype.itemsize != 4:
-                    raise TypeError("update_host needs 32-bit arrays")
-                lst.append(a.ctypes.data)
-        n = len(src)
-        self._check(lib().cbaa_update_host(self._h, C.c_void_p(ps[0]), C.c_void_p(pd[0]), n, _stream(stream)),
+                if a.dtype not in (np.dtype(np.uint32), np.dtype(np.int32)):
+                    raise TypeError(f"update_host needs int32/uint32 arrays, got {a.dtype}")
+                keep.append(a)
+                ptrs.append(a.ctypes.data)
+        if len(keep[0]) != len(keep[1]):
+            raise ValueError(f"src and dst differ in length ({len(keep[0])} vs {len(keep[1])})")
+        n = len(keep[0])
+        self._check(lib().cbaa_update_host(self._h, C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]), n, _stream(stream)),
                     "cbaa_update_host")
+        del keep
 
     def skipped(self, stream=None) -> int:
         v = C.c_uint64()

@@ -181,6 +181,9 @@ int validate(const cbaa_config* c, std::string* why) {
   uint64_t csb = 0;
   for (uint32_t a = 0; a < c->num_ra + c->num_va; ++a) csb += ((uint64_t)1 << c->cbn[a]) * c->g;
   if ((csb << c->r) / 8 > (16ull << 30) - 16) return bad("cube must be smaller than 16 GiB");
+  // reset/merge/zero-count kernels move 16-byte words and address CS slices directly: every CS must be
+  // a whole number of them (only g = 32 with a 2-column array can miss this)
+  if ((csb / 8) % 16 != 0) return bad("bytes per CS (sum of c(i)*g/8) must be a multiple of 16 (GPU word layout)");
   return CBAA_OK;
 }
 
@@ -453,10 +456,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     h->bin_ent = nullptr;
     h->bin_cap = 0;
     CK(h, cudaMalloc(&h->bin_ent, want * 4));
-    h->bin_cap = want;
     if (h->bin_log) CK(h, cudaFree(h->bin_log));
     h->bin_log = nullptr;
     CK(h, cudaMalloc(&h->bin_log, std::min(n, kChunk) * 6 + 16));   // overflow log: u32 entries | u16 bins
+    h->bin_cap = want;   // only once both buffers exist (a failed allocation is retried on the next call)
   }
   if (!h->bin_tab) {   // counts [nbins] | start [nbins + 1] | cursor [nbins · kCurStride] | log count
     CK(h, cudaMalloc(&h->bin_tab, ((2ull + kCurStride) * B.nbins + 2) * 4));

@@ -189,16 +189,17 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Geo
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint32_t skip = 0;
   const uint64_t tail0 = head + 4 * n4;
-  if (gid < head || gid < n - tail0) {
-    uint64_t k[2] = {gid, tail0 + gid};
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if ((t == 0 && gid < head) || (t == 1 && k[1] < n)) {
-        uint32_t s = src[k[t]], d = dst[k[t]];
-        if (normalize<PREFIX>(G, s, d)) set_pair_generic<MODE>(G, s, d, cube, lo, span);
-        else ++skip;
-      }
-    }
+  // scalar head [0, head) and tail [tail0, n), grid-stride: with differently aligned arrays head = n, so
+  // the whole window can take this path and may be far larger than the grid
+  for (uint64_t k = gid; k < head; k += stride) {
+    uint32_t s = src[k], d = dst[k];
+    if (normalize<PREFIX>(G, s, d)) set_pair_generic<MODE>(G, s, d, cube, lo, span);
+    else ++skip;
+  }
+  for (uint64_t k = tail0 + gid; k < n; k += stride) {
+    uint32_t s = src[k], d = dst[k];
+    if (normalize<PREFIX>(G, s, d)) set_pair_generic<MODE>(G, s, d, cube, lo, span);
+    else ++skip;
   }
   const uint32_t* s4 = src + head;
   const uint32_t* d4 = dst + head;
@@ -591,8 +592,10 @@ __global__ void __launch_bounds__(kDetThreads) k_hot(const __grid_constant__ Geo
     rec->tuples = prod;
     rec->overflow = prod > G.tuple_cap ? 1 : 0;
     // work units of the Alg. 3 kernel: every tuple (Cartesian) or every (hc0, hc1) pair (join)
-    D.units[cs] = rec->overflow ? 0ull
-                                : (join ? (unsigned long long)__ldcg(&rec->n_hot[0]) * __ldcg(&rec->n_hot[1]) : prod);
+    // (an empty HC(i) makes the tuple space empty: no units, the join would only enumerate dead pairs)
+    D.units[cs] = (rec->overflow || prod == 0)
+                      ? 0ull
+                      : (join ? (unsigned long long)__ldcg(&rec->n_hot[0]) * __ldcg(&rec->n_hot[1]) : prod);
     __threadfence();
     unsigned int old = atomicAdd(D.done_all, 1u);
     s_last_all = old == n_range - 1;   // a second flag: other warps may still be reading s_last
@@ -801,10 +804,11 @@ __global__ void __launch_bounds__(kDetThreads) k_join3(const __grid_constant__ G
       const cbaa_cs_stats* rec = D.rec + cs;
       const uint32_t n1 = __ldg(&rec->n_hot[1]);
       const uint32_t n2 = __ldg(&rec->n_hot[2]);
-      const uint32_t u = (uint32_t)(t - __ldg(D.prefix + lo));
+      const uint64_t u = t - __ldg(D.prefix + lo);   // < |HC(0)|·|HC(1)|, which can pass 2^32
       const uint32_t* hcs = D.hc + (size_t)cs * G.ra_cols;
-      hc0 = __ldg(hcs + G.ra_off[0] + u / n1);
-      hc1 = __ldg(hcs + G.ra_off[1] + u % n1);
+      const uint64_t q = u / n1;
+      hc0 = __ldg(hcs + G.ra_off[0] + (uint32_t)q);
+      hc1 = __ldg(hcs + G.ra_off[1] + (uint32_t)(u - q * n1));
       hc2list = hcs + G.ra_off[2];
       // CP(0): low cp0 bits of hc0 == top cp0 bits of hc1
       if ((hc0 & ((1u << G.cp[0]) - 1u)) == (hc1 >> (G.cbn[1] - G.cp[0]))) {

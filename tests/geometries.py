@@ -27,5 +27,7 @@ def random_params(seed, max_cube_bytes=1 << 24, g_choices=(32, 64, 128, 256)):
                  mangle_a=int(rng.integers(0, 1 << 31)) * 2 + 1, mangle_b=int(rng.integers(0, 1 << 32)),
                  bv_seed=int(rng.integers(0, 1 << 32)), va_seeds=[int(x) for x in rng.integers(0, 1 << 32, nva)],
                  theta_formula=int(rng.integers(0, 2)))
-        if O.validate(p)[0] == 0 and O.cube_bytes(p) <= max_cube_bytes:
+        # the GPU build also needs 16-byte CS slices (cbaa_config_validate); the oracle itself is generic
+        cs_bytes = O.cube_bytes(p) >> r if O.validate(p)[0] == 0 else 1
+        if O.validate(p)[0] == 0 and O.cube_bytes(p) <= max_cube_bytes and cs_bytes % 16 == 0:
             return p

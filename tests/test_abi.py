@@ -102,6 +102,11 @@ def test_validation_agrees_with_oracle():
         c = cb.config_from_dict(p)
         rc, msg = cb.validate(c)
         orc, omsg = O.validate(p)
+        if orc == 0 and (O.cube_bytes(p) >> p["r"]) % 16:
+            # the GPU build's one extra rule (16-byte CS slices); the oracle is generic
+            assert rc == cb.E_CONFIG and "multiple of 16" in msg, (p, msg)
+            n_bad += 1
+            continue
         assert (rc == 0) == (orc == 0), (p, msg, omsg)
         if rc:
             n_bad += 1

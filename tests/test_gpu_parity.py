@@ -133,6 +133,36 @@ def test_misaligned_inputs(paper, off_s, off_d):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("off_s, off_d", [(0, 1), (3, 1)])
+def test_misaligned_inputs_larger_than_grid(paper, off_s, off_d, mode):
+    """Differently aligned src/dst send every pair down the scalar path of the direct kernel; with 2M pairs
+    (far more than the persistent grid's threads) the grid-stride loop must still visit all of them."""
+    n = 2_000_000
+    src, dst = W.random_pairs(n + 4, 12)
+    big_s, big_d = dev(src), dev(dst)
+    s, d = big_s[off_s: off_s + n], big_d[off_d: off_d + n]
+    cb = handle(paper, update_mode=mode)
+    cb.reset()
+    cb.update(s, d)
+    ref, _ = O.update(paper, src[off_s: off_s + n], dst[off_d: off_d + n])
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+def test_update_host_checks(paper):
+    """update_host refuses unequal lengths and non-32-bit dtypes, and keeps converted copies alive."""
+    src, dst = W.random_pairs(100_000, 13)
+    cb = handle(paper)
+    with pytest.raises(ValueError):
+        cb.update_host(src, dst[:-1])
+    with pytest.raises(TypeError):
+        cb.update_host(src.astype(np.float32), dst)
+    cb.reset()
+    cb.update_host(src[::-1], dst[::-1].astype(np.int32))   # non-contiguous views: converted copies
+    ref, _ = O.update(paper, src[::-1].copy(), dst[::-1].copy())
+    assert np.array_equal(gpu_cube(cb), ref)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("passes", [1, 2, 3, 7])
 def test_update_passes(paper, passes, mode):
     """The address-range passes and the update mode (test-and-set vs plain RED) change
