@@ -46,6 +46,8 @@ typedef struct {
   int32_t direction;             /* 0 = normalized input, 1 = inner-prefix      */
   uint32_t n_prefix;
   uint32_t prefix[ORC_MAX_PREFIX], prefix_mask[ORC_MAX_PREFIX];
+  int32_t union_threshold;       /* Alg. 3 threshold (Q20): 0 = θ_bn of Alg. 2,
+                                    1 = union-specific θ_uc (Thm. 2 inverted)  */
 } orc_config;
 
 typedef struct {
@@ -65,7 +67,8 @@ typedef struct {
   uint64_t candidates;  /* tuples passing the CP check           */
   uint64_t hits;        /* tuples accepted by the union check    */
   int32_t overflow;     /* 1 if tuples > tuple_cap (skipped)     */
-  int32_t _pad;
+  uint32_t zmax_uc;     /* floor(θ_uc): Alg. 3 accepts Z ≤ this  */
+  double theta_uc;      /* union-column threshold of Alg. 3      */
 } orc_cs_stats;
 
 /* ---------------------------------------------------------------- hashing */
@@ -151,6 +154,7 @@ int orc_validate(const orc_config* c, char* err, int errlen) {
     if (cp[i] > ep[(i + 1) % c->num_ra]) FAIL(11, "cp(i) must be <= ep((i+1) mod num_ra) (S:39)");
   }
   if (c->theta_formula != 0 && c->theta_formula != 1) FAIL(12, "theta_formula must be 0 (paper) or 1 (inverted)");
+  if (c->union_threshold != 0 && c->union_threshold != 1) FAIL(12, "union_threshold must be 0 (same as Alg. 2) or 1 (union)");
   if (c->direction != 0 && c->direction != 1) FAIL(13, "direction must be 0 (normalized) or 1 (inner prefix)");
   if (c->n_prefix > ORC_MAX_PREFIX) FAIL(14, "at most 16 inner prefixes");
   return 0;
@@ -339,6 +343,21 @@ double orc_hot_threshold(double theta, double eps, double g, int formula) {
   return v < 0.0 ? 0.0 : v;
 }
 
+/* Union-column threshold of Alg. 3 (Q20 option).  P:309 rejects a tuple whose
+ * union column UC has more than θ_bn zero bits, reusing Alg. 2's per-column
+ * threshold although UC's noise differs.  Theorem 1
+ * gives UC's shared-bit probability ε and Theorem 2 its estimator
+ * −g·ln(Z/(g(1−ε))); solving estimate ≥ θ for Z gives
+ *   θ_uc = g·(1−ε)·e^{−θ/g},
+ * so with this option Alg. 3 accepts exactly the candidates whose Theorem 2
+ * estimate is ≥ θ (Def. 1).  Clamped at 0.  Pin: ε = 0 closed form
+ * (= Eq. 1 inverted), the golden ε ≠ 0 values, the round trip through
+ * orc_corrected_estimate, and "output = candidates with estimate ≥ θ". */
+double orc_union_threshold(double theta, double eps, double g) {
+  double v = g * (1.0 - eps) * exp(-theta / g);
+  return v < 0.0 ? 0.0 : v;
+}
+
 /* η of a CS by whole-array linear counting over RA(0) (Q12):
  * η = −c(0)·g·ln(Ztot/(c(0)·g)); Ztot = 0 → η = +∞ (ε then hits its cap). */
 void orc_cs_load(const orc_config* c, const uint8_t* cube, uint32_t cs, uint64_t* ztot_out, double* eta_out,
@@ -431,6 +450,9 @@ int orc_detect(const orc_config* c, const uint8_t* cube, double theta, orc_host*
     orc_cs_load(c, cube, cs, &st.ztot, &st.eta, &st.eps);
     st.theta_bn = orc_hot_threshold(theta, st.eps, (double)c->g, c->theta_formula);
     st.zmax = orc_zmax(st.theta_bn, c->g);
+    /* Alg. 3's threshold: the same θ_bn as written, or θ_uc (Q20) */
+    st.theta_uc = c->union_threshold ? orc_union_threshold(theta, st.eps, (double)c->g) : st.theta_bn;
+    st.zmax_uc = orc_zmax(st.theta_uc, c->g);
     orc_hot_columns(c, cube, cs, st.zmax, hc, n_hc);
     uint64_t prod = 1;
     for (uint32_t i = 0; i < c->num_ra; ++i) {
@@ -453,7 +475,7 @@ int orc_detect(const orc_config* c, const uint8_t* cube, double theta, orc_host*
         if (orc_lp_from_tuple(c, cols, &lp)) {
           st.candidates++;
           uint32_t z = orc_union_zeros(c, cube, cs, cols, lp);
-          if (z <= st.zmax) {   /* P:309 reject iff zeros > θ_bn (Q16) */
+          if (z <= st.zmax_uc) {   /* P:309 reject iff zeros > θ_bn (Q16), or θ_uc (Q20) */
             st.hits++;
             if (total == alloc) { alloc *= 2; hosts = (orc_host*)realloc(hosts, alloc * sizeof(orc_host)); }
             uint32_t m = c->r == 0 ? lp : ((lp << c->r) | cs);

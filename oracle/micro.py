@@ -150,9 +150,12 @@ class Cube:
                     for a, col in enumerate(cols):
                         rows &= self.cells.get((cs, a, col), set())
                     z = g - len(rows)
-                    if z <= zmax:
+                    est = math.inf if z == 0 else max(0.0, -g * math.log(z / (g - g * eps)))
+                    # union option (Q20): Def. 1 directly, accept iff the Thm. 2 estimate reaches θ
+                    # (the C oracle thresholds Z at floor(g(1-eps)e^(-theta/g)) instead)
+                    accept = est >= theta if p.get("union_threshold", 0) else z <= zmax
+                    if accept:
                         st["hits"] += 1
-                        est = math.inf if z == 0 else max(0.0, -g * math.log(z / (g - g * eps)))
                         ip = unmangle(p, (lp << p["r"]) | cs)
                         hosts.append((ip, cs, lp, z, est))
             stats.append(st)

@@ -40,6 +40,7 @@ class OrcConfig(C.Structure):
         ("va_seeds", C.c_uint32 * MAX_VA), ("theta_formula", C.c_int32), ("tuple_cap", C.c_uint64),
         ("direction", C.c_int32), ("n_prefix", C.c_uint32),
         ("prefix", C.c_uint32 * MAX_PREFIX), ("prefix_mask", C.c_uint32 * MAX_PREFIX),
+        ("union_threshold", C.c_int32),
     ]
 
 
@@ -51,7 +52,8 @@ class OrcHost(C.Structure):
 class OrcStats(C.Structure):
     _fields_ = [("ztot", C.c_uint64), ("eta", C.c_double), ("eps", C.c_double), ("theta_bn", C.c_double),
                 ("zmax", C.c_uint32), ("n_hot", C.c_uint32 * MAX_RA), ("tuples", C.c_uint64),
-                ("candidates", C.c_uint64), ("hits", C.c_uint64), ("overflow", C.c_int32), ("_pad", C.c_int32)]
+                ("candidates", C.c_uint64), ("hits", C.c_uint64), ("overflow", C.c_int32), ("zmax_uc", C.c_uint32),
+                ("theta_uc", C.c_double)]
 
 
 HOST_DTYPE = np.dtype([("ip", "<u4"), ("cs", "<u4"), ("lp", "<u4"), ("z", "<u4"), ("estimate", "<f8")])
@@ -78,6 +80,7 @@ def to_struct(p: dict) -> OrcConfig:
     c.theta_formula = p.get("theta_formula", 0)
     c.tuple_cap = p.get("tuple_cap", 1 << 24)
     c.direction = p.get("direction", 0)
+    c.union_threshold = p.get("union_threshold", 0)
     prefixes = p.get("prefixes", [])
     c.n_prefix = len(prefixes)
     for i, (pre, mask) in enumerate(prefixes):
@@ -120,6 +123,7 @@ def lib():
             "orc_shared_bit_prob": (dbl, [cfg, dbl]),
             "orc_corrected_estimate": (dbl, [dbl, dbl, dbl]),
             "orc_hot_threshold": (dbl, [dbl, dbl, dbl, C.c_int]),
+            "orc_union_threshold": (dbl, [dbl, dbl, dbl]),
             "orc_cs_load": (None, [cfg, C.c_void_p, u32, P(u64), P(dbl), P(dbl)]),
             "orc_zmax": (u32, [dbl, u32]),
             "orc_zero_counts_ra": (None, [cfg, C.c_void_p, C.c_void_p]),
@@ -229,6 +233,10 @@ def hot_threshold(theta, eps, g, formula=0):
     return lib().orc_hot_threshold(float(theta), float(eps), float(g), formula)
 
 
+def union_threshold(theta, eps, g):
+    return lib().orc_union_threshold(float(theta), float(eps), float(g))
+
+
 def zmax(theta_bn, g):
     return lib().orc_zmax(float(theta_bn), g)
 
@@ -289,6 +297,7 @@ def detect(p, cube, theta, cap: int = 1 << 20):
     sdicts = []
     for s in stats:
         sdicts.append(dict(ztot=s.ztot, eta=s.eta, eps=s.eps, theta_bn=s.theta_bn, zmax=s.zmax,
+                           theta_uc=s.theta_uc, zmax_uc=s.zmax_uc,
                            n_hot=list(s.n_hot[: p["num_ra"]]), tuples=s.tuples, candidates=s.candidates,
                            hits=s.hits, overflow=s.overflow))
     return st, hosts, sdicts

@@ -16,9 +16,12 @@ def tiny_window(seed, n_hosts=300, n_flows=1500, scanners=(220, 150, 400), n=800
     return W.generate(W.WindowSpec(n=n, n_hosts=n_hosts, n_flows=n_flows, scanners=scanners), seed)
 
 
+@pytest.mark.parametrize("union", [0, 1])
 @pytest.mark.parametrize("seed", range(6))
-def test_random_geometry_cube_and_detect(seed):
-    p = random_params(seed, max_cube_bytes=1 << 21, g_choices=(32, 64, 128))
+def test_random_geometry_cube_and_detect(seed, union):
+    """union = 1: the Q20 option; the C oracle thresholds Z at floor(θ_uc), the micro-oracle accepts iff the
+    Thm. 2 estimate is ≥ θ (Def. 1) — two statements of the same decision."""
+    p = dict(random_params(seed, max_cube_bytes=1 << 21, g_choices=(32, 64, 128)), union_threshold=union)
     w = tiny_window(seed)
     cube, _ = O.update(p, w.src, w.dst)
     m = micro.Cube(p)

@@ -402,3 +402,64 @@ def test_tuple_cap_overflow():
     assert any(s["overflow"] for s in stats)
     st2, hosts2, stats2 = O.detect(dict(p, tuple_cap=1 << 24), cube, 256)
     assert st2 == 0 and set(w.planted) <= set(hosts2["ip"].tolist())
+
+
+# ------------------------------------------------------------------ Q20: union-specific threshold (f4)
+def test_union_threshold_closed_form(golden):
+    """θ_uc = g(1−ε)e^{−θ/g}: Thm. 2 solved for Z at estimate = θ.  Golden values evaluated with
+    decimal arithmetic (tests/golden/union_threshold.txt); ε = 0 equals the Eq. 1 inverse (θ_bn pin);
+    feeding θ_uc back through Thm. 2 returns θ (catches a dropped (1−ε) or a sign slip); clamp at 0."""
+    for theta, eps, v in golden("union_threshold.txt")["union_thr"]:
+        assert O.union_threshold(theta, eps, 4096) == pytest.approx(v, rel=1e-13), (theta, eps)
+    assert O.union_threshold(1024, 0.0, 4096) == pytest.approx(golden("closed_forms.txt")["theta_bn"][2][1], abs=1e-9)
+    for theta in (256, 1024, 3000, 8192):
+        for eps in (0.0, 1e-4, 0.05, 0.3):
+            t = O.union_threshold(theta, eps, 4096)
+            assert O.corrected_estimate(t, eps, 4096) == pytest.approx(theta, rel=1e-12)
+    assert O.union_threshold(1024, 1.0, 4096) == 0.0
+    # against the paper's θ_bn: larger below θ = g·ln 2, smaller above (θ_bn − θ_uc = gε(2e^{−θ/g} − 1))
+    eps = 0.02
+    assert O.union_threshold(1024, eps, 4096) < O.hot_threshold(1024, eps, 4096, 0)
+    assert O.union_threshold(4096, eps, 4096) > O.hot_threshold(4096, eps, 4096, 0)
+
+
+def _loaded_window(p, seed):
+    """A window loaded enough for ε to matter (λ ≈ θ/3 per column) with hosts spread around θ."""
+    rng = np.random.default_rng(seed)
+    sc = tuple(int(x) for x in rng.integers(120, 700, 60))
+    spec = W.WindowSpec(n=260_000, n_hosts=6000, n_flows=120_000, card_cap=150, scanners=sc)
+    return W.generate(spec, seed)
+
+
+@pytest.mark.parametrize("theta", [256, 600])
+def test_union_threshold_accepts_exactly_estimate_ge_theta(theta):
+    """Q20 option: Alg. 2 (hot columns, tuples, candidates) is unchanged and Alg. 3 accepts a candidate iff
+    its Thm. 2 estimate is ≥ θ (Def. 1).  Checked per CS against the full candidate list the
+    oracle exposes (orc_candidates + orc_union_zeros), and against the paper option's output."""
+    p = small_params(r=2, g=1024, cbn=[11, 11, 10, 10], clbs=[0, 10, 20])   # L = 30: ep [10,10,10], cp [1,1,0]
+    assert O.validate(p)[0] == 0
+    w = _loaded_window(p, 3)
+    cube, _ = O.update(p, w.src, w.dst)
+    st0, h0, s0 = O.detect(p, cube, theta)
+    pu = dict(p, union_threshold=1)
+    st1, h1, s1 = O.detect(pu, cube, theta)
+    for a, b in zip(s0, s1):
+        for k in ("ztot", "eta", "eps", "theta_bn", "zmax", "n_hot", "tuples", "candidates", "overflow"):
+            assert a[k] == b[k], k
+        assert a["zmax_uc"] == a["zmax"] and b["theta_uc"] == O.union_threshold(theta, b["eps"], p["g"])
+    expect, rejected = [], 0
+    for cs in range(1 << p["r"]):
+        for lp in O.candidates(p, cube, cs, s1[cs]["zmax"]):
+            cols = [O.ra_col(p, int(lp), i) for i in range(p["num_ra"])]
+            z = O.union_zeros(p, cube, cs, cols, int(lp))
+            est = O.corrected_estimate(z, s1[cs]["eps"], p["g"])
+            if est >= theta:
+                expect.append((O.unmangle(p, (int(lp) << p["r"]) | cs), z))
+            else:
+                rejected += 1
+    assert expect and rejected   # both sides of θ are populated, so the check discriminates
+    assert sorted(expect) == sorted((int(h["ip"]), int(h["z"])) for h in h1)
+    assert all(h["estimate"] >= theta for h in h1)
+    # θ < g·ln 2 here, so θ_uc < θ_bn: the union option drops exactly the paper output's hosts below θ
+    kept = [(int(h["ip"]), int(h["z"])) for h in h0 if h["estimate"] >= theta]
+    assert kept == [(int(h["ip"]), int(h["z"])) for h in h1]
