@@ -1,15 +1,23 @@
 #!/usr/bin/env python
 """CBAA window benchmark (BASELINE.json metric: packet pairs/s per window update + window-end detect ms).
 
-One step = one window of the hot path: reset (a7) → update of the window's pairs (a0-a6) →
-[OR-merge over NVLink, a8, N > 1] → detect (a9-a14, host list filled).  Workload: BASELINE config 2
-(100M core-network-shaped pairs per GPU, Zipf hosts, ~0.1% super hosts, paper geometry, θ = 1024),
-synthetic and seeded.  Inputs (800 MB per GPU) exceed the 126 MB L2, so no extra flush.
+One step = one window of the hot path: reset (a7) → update of the window's pairs (a0-a6) → [OR-merge
+of router cubes, a8] → detect (a9-a14, host list filled).  Synthetic, seeded workloads:
 
-  python bench.py [--gpus N --steps K --warmup W]           # our CUDA path, one JSON line on rank 0
-  python bench.py --impl reference [...]                    # the CPU oracle as it stands (reference arm)
-Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; each rank is one edge router with its own
-100M-pair shard of one global window (weak scaling); max-over-ranks device time.
+  C2 (default)  BASELINE config 2: 100M core-network-shaped pairs per GPU (Zipf hosts, ~0.1 % super
+                hosts), paper geometry, θ = 1024; weak scaling (each rank one edge router with its own
+                100M-pair stream of one global flow set); windows pipelined (detect of window k beside the
+                update of window k+1, two cubes).  The last window is checked against the oracle's
+                host list (tests/golden/c2_seed1_theta1024_hosts.txt) at N = 1.
+  C3            config 3: 4 edge routers × 50M pairs of one flow set, per-router cubes OR-merged, global
+                detect; the 4 routers are spread over the N ranks (N ∈ {1, 2, 4}).
+  C4            config 4: one 2B-pair window (8 shards of 250M, planted scanners and DDoS victims),
+                strong scaling: rank p updates shards [8p/N, 8(p+1)/N) into its cube.
+  C1            config 1: the 1M-pair tiny window.
+
+  python bench.py [--gpus N --steps K --warmup W --workload C2]   # our CUDA path, one JSON line on rank 0
+  python bench.py --impl reference [...]                          # the CPU oracle as it stands
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; max-over-ranks device time.
 """
 from __future__ import annotations
 
@@ -27,25 +35,27 @@ sys.path.insert(0, ROOT)
 
 METRIC = "packet pairs/sec per window update (1/2/4/8 B200) + window-end detect ms"
 THETA = 1024
+GOLDEN_C2 = os.path.join(ROOT, "tests", "golden", "c2_seed1_theta1024_hosts.txt")
+NCU_BINNED = os.path.join(ROOT, "profiles", "r02_ncu_binned.json")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["C2", "C1"], default="C2")
+    ap.add_argument("--workload", choices=["C2", "C1", "C3", "C4"], default="C2")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--passes", type=int, default=0, help="update passes (0 = library auto)")
+    ap.add_argument("--detect-samples", type=int, default=200, help="detects timed for the latency percentiles")
+    ap.add_argument("--passes", type=int, default=0, help="direct update: address-range passes (0 = auto)")
     ap.add_argument("--update-mode", choices=["test_set", "red", "binned"], default="binned",
-                    help="binned (default): count/scatter/apply through shared memory; test_set / red: the "
+                    help="binned (default): sample/scatter/apply through shared memory; test_set / red: the "
                          "direct random-access kernel (DESIGN.md §6)")
     ap.add_argument("--no-pipeline", action="store_true",
-                    help="N=1: run windows strictly one after another (default: window k's detect overlaps "
-                         "window k+1's reset+update on a second cube and a high-priority stream)")
+                    help="C1/C2: run windows strictly one after another (default: pipelined, two cubes)")
     ap.add_argument("--exchange", choices=["nccl", "p2p", "ipc"], default="ipc",
                     help="N>1 window-end exchange: NCCL all_to_all + OR kernel, or the NVLink pull-OR over "
                          "symmetric memory (p2p) / CUDA IPC mappings (ipc)")
@@ -53,27 +63,60 @@ def parse():
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def workload(name, seed, rank, world):
-    from paper_1901_06207_b200 import workload as W
-    spec = W.C2 if name == "C2" else W.C1
-    # one global flow set (shared seed); each router sees its own packets of those flows
-    pseed = seed if world == 1 else seed * 1000 + rank + 1
-    return spec, W.generate(spec, seed, packet_seed=pseed, with_raw=False)
+# --------------------------------------------------------------------------------------- workloads
+class Plan:
+    """What one rank processes per window: a list of streams, each fed to its own router cube (C3) or all
+    into one cube (C1/C2/C4)."""
+
+    def __init__(self, name, seed, rank, world):
+        from paper_1901_06207_b200 import workload as W
+        self.name = name
+        if name in ("C1", "C2"):
+            self.spec = W.C2 if name == "C2" else W.C1
+            # one global flow set (shared seed); each router sees its own packets of those flows (P:78)
+            self.units = [("router", seed if world == 1 else seed * 1000 + rank + 1)]
+            self.scaling, self.per_router_cube = "weak", False
+            self.global_pairs = self.spec.n * world
+            self.desc = (f"{name}: {self.spec.n // 1_000_000}M pairs/GPU, {self.spec.n_hosts} inner hosts, "
+                         f"{self.spec.n_flows / 1e6:.1f}M Zipf(s={self.spec.zipf_s}) flows, shuffled")
+        elif name == "C3":
+            if 4 % world:
+                raise SystemExit("C3 has 4 edge routers: run it on N ∈ {1, 2, 4} GPUs")
+            self.spec = W.C3_ROUTER
+            self.units = [("router", k + 1) for k in range(rank * 4 // world, (rank + 1) * 4 // world)]
+            self.scaling, self.per_router_cube = "weak", True
+            self.global_pairs = 4 * self.spec.n
+            self.desc = "C3: 4 edge routers x 50M pairs of one C2-like flow set, router cubes OR-merged (P:249)"
+        else:   # C4
+            if 8 % world:
+                raise SystemExit("C4 has 8 shards: run it on N ∈ {1, 2, 4, 8} GPUs")
+            self.spec = W.c4_spec()
+            self.units = [("shard", j + 1) for j in range(rank * 8 // world, (rank + 1) * 8 // world)]
+            self.scaling, self.per_router_cube = "strong", False
+            self.global_pairs = 8 * self.spec.n
+            self.desc = ("C4: one 2B-pair window (8 shards x 250M, 16M Zipf flows over 1.2M hosts, 50 scanners, "
+                         "20 DDoS victims with 5% of the packets), strong scaling over the ranks")
+        self.seed = seed if name != "C4" else 4
+
+    def generate(self, k):
+        """Host arrays (src, dst) of unit k of this rank."""
+        from paper_1901_06207_b200 import workload as W
+        w = W.generate(self.spec, self.seed, packet_seed=self.units[k][1], with_raw=False)
+        return w.src, w.dst
+
+    @property
+    def rank_pairs(self):
+        return self.spec.n * len(self.units)
 
 
-def config_block(name, spec, world):
-    return {"workload": f"{name}: {spec.n // 1_000_000}M pairs/GPU, {spec.n_hosts} inner hosts, "
-                        f"{spec.n_flows / 1e6:.1f}M Zipf(s={spec.zipf_s}) flows, shuffled",
-            "pairs_per_gpu": spec.n, "global_pairs": spec.n * world,
+def config_block(plan, world, exchange):
+    return {"workload": plan.desc, "pairs_per_gpu": plan.rank_pairs, "global_pairs": plan.global_pairs,
             "geometry": "r=4 |RA|=3 |VA|=1 g=4096 c=4096 (128 MiB cube, P:437)", "theta": THETA,
-            "parallelism": f"routers{world}" if world > 1 else "single",
-            "l2": "inputs 800 MB/GPU > 126 MB L2 (no extra flush); cube reset each window"}
+            "parallelism": f"routers{world}" if world > 1 else "single", "exchange": exchange,
+            "l2": "inputs (>= 400 MB/GPU) exceed the 126 MB L2, no extra flush; cube reset each window"}
 
 
 # --------------------------------------------------------------------------------------- clocks
@@ -104,7 +147,7 @@ class ClockSampler:
                         self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.N:
@@ -124,9 +167,10 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# --------------------------------------------------------------------------------------- peaks / profiles
 def access_peaks():
-    """Measured random single-word access rates over an L2-resident 64 MiB buffer (tools/redbench --quick):
-    {"red": RED.OR/s, "ldg": 32-bit loads/s}.  The update touches one random word per bit it sets."""
+    """Measured random single-word access rates over an L2-resident 64 MiB buffer (tools/redbench --quick,
+    run in this process before the timed region): {"red": RED.OR/s, "ldg": loads/s, "ldg_ca": ...}."""
     exe = os.path.join(ROOT, "tools", "redbench")
     peaks = {}
     try:
@@ -147,84 +191,139 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic():
-    try:
-        return json.load(open(os.path.join(ROOT, "profiles", "ncu_update_traffic.json")))
-    except Exception:
-        return None
-
-
 def ncu_binned():
-    """DRAM bytes per launch of the binned-update kernels from the committed ncu --set full capture."""
+    """Per-launch DRAM bytes and issued L2 REDs of the update kernels from the committed ncu capture."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_binned.json")))
+        return json.load(open(NCU_BINNED))
     except Exception:
         return {}
 
 
-def ncu_update_counters():
-    """Per-launch L1/L2 utilisation of k_update from the committed ncu --set full capture."""
+def cpu_info():
+    info = {"threads": os.cpu_count()}
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_counters.json")))
-        ls = [e for e in d["launches"] if "k_update" in e["kernel"]]
-        keys = ("lts_throughput_avg_pct", "lts_throughput_max_pct", "l1tex_throughput_pct", "l1_hit_pct", "l2_hit_pct")
-        return {k: [round(e[k], 1) for e in ls] for k in keys} | {"source": "profiles/r01_ncu_counters.json"}
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k in ("Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.lower().replace("(s)", "s").replace(" ", "_")] = int(v)
     except Exception:
-        return None
+        pass
+    return info
 
 
-# --------------------------------------------------------------------------------------- reference arm
+# --------------------------------------------------------------------------------------- the oracle on the host
+def oracle_window(blocks, threads):
+    """The oracle as it stands over one window: `threads` workers each run oracle update (Alg. 1) on a
+    contiguous block into a private cube, the cubes are OR-merged with the oracle's merge (the shard-OR
+    invariant), then the oracle's detect.  Returns (update_s, detect_s, pairs, hosts)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from oracle import oracle as O
+    p = O.default_params()
+    src = np.concatenate([b[0] for b in blocks]) if len(blocks) > 1 else blocks[0][0]
+    dst = np.concatenate([b[1] for b in blocks]) if len(blocks) > 1 else blocks[0][1]
+    n = src.size
+    cuts = [n * t // threads for t in range(threads + 1)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:   # ctypes releases the GIL inside the oracle
+        cubes = list(ex.map(lambda t: O.update(p, src[cuts[t]:cuts[t + 1]], dst[cuts[t]:cuts[t + 1]])[0],
+                            range(threads)))
+    for c in cubes[1:]:
+        O.merge(cubes[0], c)
+    t1 = time.perf_counter()
+    _, hosts, _ = O.detect(p, cubes[0], THETA)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, n, hosts
+
+
+def cpu_baseline(blocks):
+    """Oracle timings on the host cores (rank 0, N = 1): single-threaded on a 20M-pair sample, and with
+    T = nproc threads (private cubes OR-merged) on the whole window; update and detect separately."""
+    info = cpu_info()
+    T = info["threads"] or 1
+    m = min(20_000_000, blocks[0][0].size)
+    u1, d1, n1, _ = oracle_window([(blocks[0][0][:m], blocks[0][1][:m])], 1)
+    uT, dT, nT, _ = oracle_window(blocks, T)
+    return {"value": nT / (uT + dT), "unit": "pairs/s", "cores": T, "kind": "oracle",
+            "sample": f"whole window ({nT} pairs): oracle update on {T} threads (private cubes OR-merged) "
+                      f"{uT:.2f} s + oracle detect {dT:.2f} s (θ={THETA})",
+            "threads_T": {"threads": T, "pairs": nT, "update_s": uT, "detect_s": dT,
+                          "update_pairs_per_s": nT / uT},
+            "single_thread": {"threads": 1, "pairs": n1, "update_s": u1, "detect_s": d1,
+                              "update_pairs_per_s": n1 / u1,
+                              "sample": f"first {n1} pairs of the window (update), detect of that cube"},
+            "cpu": info}
+
+
 def run_reference(args):
+    """Reference arm: the oracle as it stands on the same workload, T = nproc threads (rank 0 only)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import oracle as O
-    spec, w = workload(args.workload, args.seed, 0, 1)
-    p = O.default_params()
-    m = 1_000_000 if spec.n >= 1_000_000 else spec.n
-    times = []
+    plan = Plan(args.workload, args.seed, 0, 1)
+    # C4: the whole 2B-pair window would take minutes per step on the host; one 250M shard per step
+    nunits = 1 if args.workload == "C4" else len(plan.units)
+    blocks = [plan.generate(k) for k in range(nunits)]
+    T = os.cpu_count() or 1
+    times, ups, dets = [], [], []
+    n = 0
     for k in range(args.warmup + args.steps):
-        off = (k * m) % max(1, spec.n - m + 1)
-        t0 = time.perf_counter()
-        cube, _ = O.update(p, w.src[off:off + m], w.dst[off:off + m])
-        O.detect(p, cube, THETA)
-        t1 = time.perf_counter()
+        u, d, n, _ = oracle_window(blocks, T)
         if k >= args.warmup:
-            times.append(t1 - t0)
+            times.append(u + d)
+            ups.append(u)
+            dets.append(d)
     tot = sum(times)
-    value = m * len(times) / tot
-    sample = f"{m} consecutive pairs of the {args.workload} window per step (update + detect, θ={THETA})"
+    value = n * len(times) / tot
+    sample = (f"{'first shard (250M pairs) of the 2B window' if args.workload == 'C4' else 'the whole window'} "
+              f"per step: oracle update on {T} threads (private cubes OR-merged) + oracle detect (θ={THETA})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config_block(args.workload, spec, 1),
-            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "higher_is_better": True, "scaling": plan.scaling, "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": config_block(plan, 1, "none"),
+            "update_ms": 1e3 * statistics.median(ups), "detect_ms": 1e3 * statistics.median(dets),
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": T, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_info()},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(w, seconds_budget=20.0):
-    """The oracle as it stands, single-threaded, on a bounded sample of the same window."""
-    from oracle import oracle as O
-    p = O.default_params()
-    m = min(w.src.size, 60_000_000)   # ~10-15 s of single-thread oracle work on the box's CPU
-    t0 = time.perf_counter()
-    cube, _ = O.update(p, w.src[:m], w.dst[:m])
-    O.detect(p, cube, THETA)
-    t1 = time.perf_counter()
-    return {"value": m / (t1 - t0), "unit": "pairs/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {m} pairs of the window: oracle update + detect (θ={THETA}), {t1 - t0:.1f} s"}
-
-
 # --------------------------------------------------------------------------------------- our arm
 def _allreduce(v: float, op) -> float:
-    """Scalar all-reduce (max over ranks for times) on the process group's own device kind."""
     import torch
     import torch.distributed as dist
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, int(round(q / 100.0 * (len(xs) - 1))))]
+
+
+def golden_check(hosts):
+    """Compare a host list with the oracle's list of the same window (tests/golden, tools/make_golden_c2.py):
+    (ip, cs, lp, Z) exact and in order, estimates within 1e-12 relative (+inf exact)."""
+    import math
+    rows = []
+    for line in open(GOLDEN_C2):
+        if line.startswith("#") or not line.strip():
+            continue
+        ip, cs, lp, z, est = line.split()
+        rows.append((int(ip, 16), int(cs), int(lp), int(z), float(est)))
+    got = [(int(h["ip"]), int(h["cs"]), int(h["lp"]), int(h["z"]), float(h["estimate"])) for h in hosts]
+    ok = len(got) == len(rows) and all(
+        a[:4] == b[:4] and (a[4] == b[4] if math.isinf(b[4]) else abs(a[4] - b[4]) <= 1e-12 * max(1.0, abs(b[4])))
+        for a, b in zip(got, rows))
+    return {"golden": os.path.relpath(GOLDEN_C2, ROOT), "hosts": len(got), "oracle_hosts": len(rows), "match": ok}
 
 
 def main():
@@ -236,7 +335,8 @@ def main():
     import torch.distributed as dist
 
     from paper_1901_06207_b200 import distributed as D
-    from paper_1901_06207_b200.cbaa import Cbaa, default_config
+    from paper_1901_06207_b200.cbaa import Cbaa, cube_bytes, default_config
+    from paper_1901_06207_b200.pipeline import WindowPipeline
 
     rank, world, local = dist_env()
     # one GPU per rank; more ranks than GPUs (functional runs on a 1-GPU box) wrap around and then
@@ -246,24 +346,32 @@ def main():
         backend = os.environ.get("CBAA_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
     torch.cuda.set_device(local)
-    peaks_acc = access_peaks() if rank == 0 and args.update_mode != "binned" else {}
-    spec, w = workload(args.workload, args.seed, rank, world)
-    n = spec.n
-    src = torch.from_numpy(w.src.view(np.int32)).cuda()
-    dst = torch.from_numpy(w.dst.view(np.int32)).cuda()
+    peaks_acc = access_peaks() if rank == 0 else {}
+    plan = Plan(args.workload, args.seed, rank, world)
+    # inputs: device-resident per unit (host copies kept only where e2e / the CPU baseline need them)
+    keep_host = args.workload != "C4"
+    host_blocks, dev_blocks = [], []
+    for k in range(len(plan.units)):
+        s, d = plan.generate(k)
+        dev_blocks.append((torch.from_numpy(s.view(np.int32)).cuda(), torch.from_numpy(d.view(np.int32)).cuda()))
+        if keep_host or (k == 0 and rank == 0):
+            host_blocks.append((s, d))
+        del s, d
+    n = plan.rank_pairs
     cfg = default_config()
     cfg.update_passes = args.passes
     cfg.update_mode = {"test_set": 0, "red": 1, "binned": 2}[args.update_mode]
-    from paper_1901_06207_b200.cbaa import cube_bytes
-    peer = None
     exchange = args.exchange if world > 1 else "none"
+    peer = None
     if exchange == "p2p":
         try:
             peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", local))
         except Exception as e:   # no symmetric memory on this box: say so and use NCCL
             print(f"[bench] p2p exchange unavailable ({e}); using nccl", file=sys.stderr)
             exchange = "nccl"
-    cb = Cbaa(cfg, local, cube=peer.buf if peer else None)
+    nh = len(plan.units) if plan.per_router_cube else 1
+    cbs = [Cbaa(cfg, local, cube=peer.buf if (peer and j == 0) else None) for j in range(nh)]
+    cb = cbs[0]
     if exchange == "ipc":
         # collective fallback: every rank must be able to map every peer cube, else all use NCCL
         err = None
@@ -281,267 +389,267 @@ def main():
     stream = torch.cuda.Stream()
     cube_view = cb.cube()
 
-    def merge_slices(peers, lo, hi):
-        cb.merge_slice(peers, lo, hi, stream=stream)
-
-    def window(ev=None):
-        cb.reset(stream)
-        if ev:
-            ev[0].record(stream)
-        cb.update(src, dst, stream)
-        if ev:
-            ev[1].record(stream)
+    def exchange_and_detect(s):
         lo, hi = 0, n_cs
         if world > 1:
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(s):
                 if peer:
-                    lo, hi = peer.exchange(cb, rank, world, n_cs, cs_bytes, stream)
+                    lo, hi = peer.exchange(cb, rank, world, n_cs, cs_bytes, s)
                 else:
-                    lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes, merge_slices)
-        hosts, _, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=stream, with_stats=False)
+                    lo, hi = D.exchange_owned(cube_view, rank, world, n_cs, cs_bytes,
+                                              lambda ps, a, b: cb.merge_slice(ps, a, b, stream=s))
+        hosts, _, rc = cb.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s, with_stats=False)
         if exchange == "p2p":
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(s):
                 peer.window_done()
         elif exchange == "ipc":
-            peer.window_done(stream)
+            peer.window_done(s)
+        return hosts
+
+    def window(ev=None):
+        """Serial window: reset, update every unit (per-router cubes OR-merged), exchange, detect."""
+        for c in cbs:
+            c.reset(stream)
+        if ev:
+            ev[0].record(stream)
+        for j, (s, d) in enumerate(dev_blocks):
+            cbs[j if plan.per_router_cube else 0].update(s, d, stream)
+        if len(cbs) > 1:
+            cb.merge(cbs[1:], stream)
+        if ev:
+            ev[1].record(stream)
+        hosts = exchange_and_detect(stream)
         if ev:
             ev[2].record(stream)
         return D.gather_hosts(hosts, rank, world)
 
-    with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):   # at least 3 untimed warm-up windows
-            window()
-    torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = cb.kernel_launches
-    cb.set_phase_timing(True)       # event pair around every update kernel, on its stream
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_start.record(stream)
-        for k in range(args.steps):
-            hosts = window(evs[k])
-        t_end.record(stream)
+    def launches():
+        return sum(c.kernel_launches for c in cbs)
+
+    pipelined = (not args.no_pipeline and args.workload in ("C1", "C2") and args.update_mode == "binned"
+                 and (world == 1 or exchange == "ipc"))
+    if not pipelined:
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):   # at least 3 untimed warm-up windows
+                window()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = cb.kernel_launches - launches0
-    phase_ms, phase_calls = cb.update_phase_ms()
-    cb.set_phase_timing(False)
-    elapsed_ms = t_start.elapsed_time(t_end)
-    upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    post_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    if world > 1:
-        elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
-    serial_ms = elapsed_ms
-
-    # Pipelined windows (N = 1): two cubes; window k's reset+update run on the update stream while
-    # window k-1's detect runs on a high-priority stream (its 128-thread CTAs fit beside the persistent
-    # update CTAs).  Cube k%2 is reset only after the detect of window k-2 has returned (host order).
-    # Pipelined windows: two cubes; window k's reset+update run on the update stream while window k-1's
-    # [exchange +] detect runs on a high-priority stream (its kernels fit beside the persistent update
-    # CTAs).  Cube k%2 is reset only after the detect of window k-2 has returned on every rank (host
-    # order; at N > 1 the ipc exchange's window_done barrier).  N > 1 pipelines with the ipc exchange.
-    pipelined = not args.no_pipeline and (world == 1 or exchange == "ipc")
-    if pipelined:
-        cfg.detect_overlap = 1             # window-end kernels without shared memory: they co-run
-        cbs = [Cbaa(cfg, local), Cbaa(cfg, local)]
-        cb2 = cbs[1]
-        peers = [D.IpcExchange(c, rank, world) for c in cbs] if world > 1 else [None, None]
-        lo_pri, hi_pri = torch.cuda.Stream.priority_range()
-        s_upd, s_det = stream, torch.cuda.Stream(priority=hi_pri)
-
-        # the window reset moves to the detect stream: cube k%2 is cleared right after its detect (and,
-        # at N > 1, after every peer has finished reading it), overlapping the other cube's update
-        clean = [torch.cuda.Event(), torch.cuda.Event()]
-        for i, c in enumerate(cbs):
-            c.reset(s_det)
-            clean[i].record(s_det)
-
-        def finish(c, pe, px, i):
-            s_det.wait_event(pe)
-            lo, hi = 0, n_cs
-            if px:
-                lo, hi = px.exchange(c, rank, world, n_cs, cs_bytes, s_det)
-            out, _, _ = c.detect(THETA, cs_lo=lo, cs_hi=hi, stream=s_det, with_stats=False)
-            if px:
-                px.window_done(s_det)
-            c.reset(s_det)
-            clean[i].record(s_det)
-            return D.gather_hosts(out, rank, world)
-
-        def run_pipelined(n_win, upd_evs=None):
-            pending, out = None, None
-            for k in range(n_win):
-                c = cbs[k % 2]
-                s_upd.wait_event(clean[k % 2])
-                if upd_evs:
-                    upd_evs[k][0].record(s_upd)
-                c.update(src, dst, s_upd)
-                done = torch.cuda.Event()
-                done.record(s_upd)
-                if upd_evs:
-                    upd_evs[k][1].record(s_upd)
-                if pending:
-                    out = finish(*pending)
-                pending = (c, done, peers[k % 2], k % 2)
-            return finish(*pending)
-
-        run_pipelined(max(args.warmup, 3))
-        torch.cuda.synchronize()
-        launches0 = cbs[0].kernel_launches + cb2.kernel_launches
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = launches()
         for c in cbs:
-            c.set_phase_timing(True)
-        pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-        p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.set_phase_timing(True)       # event pair around every update kernel, on its stream
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            p_start.record(s_upd)
-            hosts = run_pipelined(args.steps, pevs)
-            p_end.record(s_det)
+            t_start.record(stream)
+            for k in range(args.steps):
+                hosts = window(evs[k])
+            t_end.record(stream)
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        launches = cbs[0].kernel_launches + cb2.kernel_launches - launches0
+        nlaunch = launches() - launches0
         phase_ms, phase_calls = [0.0] * 4, 0
         for c in cbs:
-            ms_c, calls_c = c.update_phase_ms()
-            phase_ms = [a + b for a, b in zip(phase_ms, ms_c)]
-            phase_calls += calls_c
+            m, k_ = c.update_phase_ms()
+            phase_ms = [a + b for a, b in zip(phase_ms, m)]
+            phase_calls += k_
             c.set_phase_timing(False)
-        elapsed_ms = p_start.elapsed_time(p_end)
+        elapsed_ms = t_start.elapsed_time(t_end)
+        upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+        lat_handle = cb
+        schedule = "serial: reset, update, [merge, exchange], detect"
+    else:
+        # the object tests/test_gpu_measured.py checks against the oracle window by window
+        pipe = WindowPipeline(cfg, local, THETA, rank=rank, world=world, update_stream=stream,
+                              gather=lambda h: D.gather_hosts(h, rank, world))
         if world > 1:
-            elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
-        upd_ms = [e[0].elapsed_time(e[1]) for e in pevs]
-        for px in peers:
-            if px:
-                px.close()
-
-    # window-end detect latency alone: update finished, then detect until the host list is filled
-    det_ms = []
-    with torch.cuda.stream(stream):
-        for _ in range(10):
+            pipe.set_exchanges([D.IpcExchange(c, rank, world) for c in pipe.cbs])
+        s0, d0 = dev_blocks[0]
+        for _ in range(max(args.warmup, 3)):
+            pipe.submit(s0, d0)
+        pipe.flush()
+        torch.cuda.synchronize()
+        launches0 = pipe.kernel_launches
+        for c in pipe.cbs:
+            c.set_phase_timing(True)
+        pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            t_start.record(pipe.s_upd)
+            for k in range(args.steps):
+                pipe.submit(s0, d0, pevs[k])
+            hosts = pipe.flush()
+            t_end.record(pipe.s_det)
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            h, _, _ = cb.detect(THETA, stream=stream, with_stats=False)
-            det_ms.append(1e3 * (time.perf_counter() - t0))
-
-    e2e = None
-    if not args.no_e2e:
-        ps = torch.from_numpy(w.src.view(np.int32)).pin_memory()
-        pd = torch.from_numpy(w.dst.view(np.int32)).pin_memory()
-        ke = min(args.steps, 5)
+        if world > 1:
+            dist.barrier()
+        nlaunch = pipe.kernel_launches - launches0
+        phase_ms, phase_calls = [0.0] * 4, 0
+        for c in pipe.cbs:
+            m, k_ = c.update_phase_ms()
+            phase_ms = [a + b for a, b in zip(phase_ms, m)]
+            phase_calls += k_
+            c.set_phase_timing(False)
+        elapsed_ms = t_start.elapsed_time(t_end)
+        upd_ms = [e[0].elapsed_time(e[1]) for e in pevs]
+        # the detect-latency samples below run on a window of the measured configuration
+        lat_handle = pipe.cbs[0]
         with torch.cuda.stream(stream):
-            cb.reset(stream)
-            cb.update_host(ps, pd, stream)
-            cb.detect(THETA, stream=stream)
+            lat_handle.reset(stream)
+            lat_handle.update(s0, d0, stream)
+        if world > 1:
+            for px in pipe.exchanges:
+                px.close()
+            with torch.cuda.stream(stream):
+                window()                  # N > 1: the latency below includes the exchange on this cube
+            lat_handle = cb
+        schedule = "pipelined: detect(k) + reset on a high-priority stream beside update(k+1), two cubes"
+    if world > 1:
+        elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
+
+    # ---- window-end detect latency: update finished → host list filled (incl. the exchange at N > 1)
+    torch.cuda.synchronize()
+    det_host, det_dev = [], []
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.detect_samples):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a_ev.record(stream)
+        if world > 1:
+            exchange_and_detect(stream)
+        else:
+            lat_handle.detect(THETA, stream=stream, with_stats=False)
+        b_ev.record(stream)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        det_host.append(1e3 * (t1 - t0))
+        det_dev.append(a_ev.elapsed_time(b_ev))
+    detect = {"p50_ms": pct(det_host, 50), "p99_ms": pct(det_host, 99), "max_ms": max(det_host),
+              "device_p50_ms": pct(det_dev, 50), "device_p99_ms": pct(det_dev, 99), "samples": len(det_host),
+              "includes_exchange": world > 1,
+              "clock": "host perf_counter around the detect call (it returns with the host list filled); "
+                       "device: CUDA events on the detect stream",
+              "target_ms": 10.0}
+    if world > 1:
+        detect["p99_ms_max_over_ranks"] = _allreduce(detect["p99_ms"], dist.ReduceOp.MAX)
+
+    # ---- end to end through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e and keep_host:
+        pinned = [(torch.from_numpy(s.view(np.int32)).pin_memory(), torch.from_numpy(d.view(np.int32)).pin_memory())
+                  for s, d in host_blocks]
+        ke = min(args.steps, 5)
+
+        def e2e_window():
+            for c in cbs:
+                c.reset(stream)
+            for j, (ps, pd) in enumerate(pinned):
+                cbs[j if plan.per_router_cube else 0].update_host(ps, pd, stream)   # H2D inside
+            if len(cbs) > 1:
+                cb.merge(cbs[1:], stream)
+            return exchange_and_detect(stream)                                     # D2H of the result
+
+        with torch.cuda.stream(stream):
+            e2e_window()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            nh = 0
             a.record(stream)
             for _ in range(ke):
-                cb.reset(stream)
-                cb.update_host(ps, pd, stream)     # pinned host → device inside the timed region
-                hh, st, _ = cb.detect(THETA, stream=stream)   # device → host of the result
-                nh = len(hh)
+                hh = e2e_window()
             b.record(stream)
             torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / ke
         if world > 1:
             e2e_ms = _allreduce(e2e_ms, dist.ReduceOp.MAX)
-        e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 24 * nh + 104 * n_cs + 8,
-               "path": "cbaa_update_host (pinned, double-buffered chunks) + cbaa_detect"}
+        e2e = {"value": plan.rank_pairs * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 24 * len(hh) + 8,
+               "path": "cbaa_update_host (pinned, double-buffered chunks) + [cbaa_merge] + cbaa_detect"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     ms_step = elapsed_ms / args.steps
-    value = n * world * args.steps / (elapsed_ms / 1e3)
+    global_pairs = plan.rank_pairs * world if plan.scaling == "weak" else plan.global_pairs
+    value = global_pairs * args.steps / (elapsed_ms / 1e3)
     upd = statistics.median(upd_ms)
-    passes = cb.update_passes
     peaks = measured_peaks()
-    hbm = peaks.get("hbm_gbs", 6650.0)
+    hbm = peaks.get("hbm_gbs", 6550.0)
     per_call = [t / max(1, phase_calls) for t in phase_ms]
-    binned = args.update_mode == "binned"
-    if binned:
-        # binned update (binned.cuh): algorithmic DRAM bytes of each kernel per launch
-        nb = ncu_binned()
-        # scatter kernel: tile sort k_bin_scatter unless CBAA_BIN_SCATTER=wc (the library's rule)
+    per_call_pairs = n / max(1, phase_calls / max(1, args.steps))   # pairs per update call
+    red_peak = peaks_acc.get("red")
+    algo_in = 8 * n                       # §8(d): 8 B of input per pair
+    algo_bits = 4 * n                     # §8(d): |RA|+|VA| = 4 single-bit ORs per pair
+    nb = ncu_binned()
+    update_block = {
+        "update_ms": upd, "pairs": n,
+        "input_hbm": {"achieved_gbs": algo_in / (upd / 1e3) / 1e9, "peak_gbs": hbm,
+                      "frac": algo_in / (upd / 1e3) / 1e9 / hbm,
+                      "note": "8 B/pair input stream over the whole update (all kernels), SURVEY 8(d)"},
+        "l2_red": {"algorithmic_bitsets_per_s": algo_bits / (upd / 1e3), "red_peak_per_s": red_peak,
+                   "frac": (algo_bits / (upd / 1e3) / red_peak) if red_peak else None,
+                   "issued_l2_reds_per_update": (nb.get("update") or {}).get("l2_red_requests"),
+                   "issued_l2_red_sectors_per_update": (nb.get("update") or {}).get("l2_red_sectors"),
+                   "note": "4 bit-sets/pair / update time vs tools/redbench --quick RED.OR peak (random unique "
+                           "words, 64 MiB L2-resident) measured in this run; > 1 means the design sets more "
+                           "bits per second than one L2 RED each could (binned: ORs done in shared memory)"},
+        "dram": {"bytes_per_update": (nb.get("update") or {}).get("dram_bytes"),
+                 "algorithmic_bytes": algo_in,
+                 "ratio": ((nb.get("update") or {}).get("dram_bytes") or 0) / algo_in if nb.get("update") else None,
+                 "source": os.path.relpath(NCU_BINNED, ROOT)},
+    }
+    if args.update_mode == "binned":
         scat = "k_bin_wc" if os.environ.get("CBAA_BIN_SCATTER") == "wc" else "k_bin_scatter"
-        # region sizing: a 1/16 sample (k_bin_sample) for chunks of ≥ 2^24 pairs with the tile scatter,
-        # else the exact count (k_bin_count) — the library's rule (cbaa.cu update_binned)
-        samp = (scat == "k_bin_scatter" and os.environ.get("CBAA_BIN_SAMPLE", "9") != "0"
-                and n >= int(os.environ.get("CBAA_BIN_SAMPLE_MIN", str(1 << 24))))
-        lg = int(os.environ.get("CBAA_BIN_SAMPLE", "9"))
-        cnt = ("k_bin_sample", 8 * 8 * (n >> lg)) if samp else ("k_bin_count", 8 * n)
-        algo = {cnt[0]: cnt[1], "k_bin_starts": 3 * 4 * 4096, scat: 12 * n,
-                "k_bin_apply": 4 * n + cb.nbytes}
+        names = ["k_bin_sample|k_bin_count", "k_bin_starts", scat, "k_bin_apply"]
         kernels = {}
-        for name, t in zip(algo, per_call):
-            kernels[name] = {"ms": t, "share": t / max(1e-9, sum(per_call)), "algorithmic_bytes": algo[name],
-                             "gbs": algo[name] / (t / 1e3) / 1e9 if t > 0 else None,
-                             "frac_hbm": algo[name] / (t / 1e3) / 1e9 / hbm if t > 0 else None,
-                             "ncu_dram_bytes": (nb.get(name) or {}).get("dram_bytes_per_launch")}
-        dom = max(kernels, key=lambda k: kernels[k]["ms"])
-        kd = kernels[dom]
-        roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
-                    "frac": kd["frac_hbm"], "traffic": kd["ncu_dram_bytes"],
-                    "algorithmic": {cnt[0]: "8 B/pair read" + (f" for 8 of every {1 << lg} pairs" if samp else ""),
-                                    scat: "8 B/pair read + 4 B/pair entry written",
-                                    "k_bin_apply": "4 B/pair entry read + the cube's words OR-ed once (+ overflow "
-                                                   "log, normally empty)"},
-                    "per_launch_ms": kd["ms"], "timing": "CUDA event pair around every update kernel on its launch "
-                    "stream over the timed region (cbaa_set_phase_timing), averaged per update call",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernels": kernels,
-                    "update_ms": upd, "update_mode": args.update_mode,
-                    "traffic_source": "profiles/r01_ncu_binned.json (ncu --set full, dram__bytes_read+write)",
-                    "limiter": "the dominant binned kernel is not DRAM-bound (ncu DRAM traffic = its algorithmic "
-                                "bytes): k_bin_scatter is issue/latency-bound (ATOMS rank, per-tile bin scan, "
-                                "4 barriers per 8192-pair tile, 16 warps/SM at 119 registers), k_bin_apply is "
-                                "shared-memory-bound (4 random LDS tests per entry); see DESIGN.md section 6"}
-        roofline_hbm = None
+        for name, t in zip(names, per_call):
+            kernels[name] = {"ms": t, "share": t / max(1e-9, sum(per_call))}
+        tsc = per_call[2]
+        design = {"k_bin_scatter": 12, "k_bin_wc": 12}[scat]
+        roofline = {"kernel": scat, "bound": "hbm",
+                    "achieved": 8 * per_call_pairs / (tsc / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": 8 * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,
+                    "traffic": (nb.get(scat) or {}).get("dram_bytes_per_launch"),
+                    "algorithmic": "SURVEY 8(d): 8 B/pair of input read per launch (pairs per launch x 8 B)",
+                    "design_bytes_per_pair": design,
+                    "design_frac": design * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,
+                    "design_note": "the binned design also writes a 4 B entry per pair (read back by k_bin_apply)",
+                    "per_launch_ms": tsc,
+                    "timing": "CUDA event pair around every update kernel on its launch stream over the timed "
+                              "region (cbaa_set_phase_timing), averaged per launch",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6550 GB/s",
+                    "kernels": kernels, "update": update_block}
     else:
-        algo = 4 * n                       # |RA|+|VA| = 4 bit-sets per pair, one random word each
-        achieved = algo / (upd / 1e3)
         peak_acc = max(peaks_acc.values()) if peaks_acc else None
-        traffic = ncu_traffic()
-        roofline = {"kernel": "k_update (cbaa_update, all passes)", "bound": "lsu_random_word",
-                    "achieved": achieved / 1e9, "peak": (peak_acc or float("nan")) / 1e9, "unit": "G word-updates/s",
-                    "frac": achieved / peak_acc if peak_acc else None,
-                    "traffic": (traffic or {}).get("dram_bytes_per_update"),
-                    "algorithmic": f"4 random 32-bit word updates per pair (one per RA/VA bit, Alg. 1) x {n} pairs "
-                                   f"per update; {passes} address-range launches",
-                    "peak_source": "tools/redbench --quick in this run: best of random 32-bit LDG (L2 / L1-cached) "
-                                   "and RED.OR over a 64 MiB L2-resident buffer (not in MEASURED_PEAKS.json)",
-                    "peak_ldg": peaks_acc.get("ldg", 0) / 1e9, "peak_ldg_ca": peaks_acc.get("ldg_ca", 0) / 1e9,
-                    "peak_red": peaks_acc.get("red", 0) / 1e9,
-                    "update_ms": upd, "launch_ms": per_call[0] / max(1, passes), "update_passes": passes,
-                    "update_mode": args.update_mode, "ncu_per_pass": ncu_update_counters()}
-        roofline_hbm = {"bound": "hbm", "achieved": 8 * n / (upd / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                        "frac": 8 * n / (upd / 1e3) / 1e9 / hbm,
-                        "note": "input stream, 8 B/pair algorithmic; peak = MEASURED_PEAKS.json hbm_gbs"}
+        achieved = algo_bits / (upd / 1e3)
+        roofline = {"kernel": "k_update", "bound": "lsu_random_word", "achieved": achieved / 1e9,
+                    "peak": (peak_acc or float("nan")) / 1e9, "unit": "G word-updates/s",
+                    "frac": achieved / peak_acc if peak_acc else None, "traffic": None,
+                    "peak_source": "tools/redbench --quick in this run (best of random LDG / RED.OR)",
+                    "update": update_block}
     line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": dict(config_block(args.workload, spec, world), exchange=exchange),
-            "detect_ms": statistics.median(det_ms), "update_ms": upd,
-            "post_update_ms": statistics.median(post_ms),
-            "windows": ("pipelined: [exchange +] detect(k) + reset overlap update(k+1), two cubes" if pipelined
-                        else "serial"),
-            "ms_per_step_serial": serial_ms / args.steps,
-            "update_pairs_per_s": n * world / (upd / 1e3),
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": plan.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config_block(plan, world, exchange), "windows": schedule,
+            "update_ms": upd, "update_pairs_per_s": n / (upd / 1e3),
+            "detect_ms": detect["p50_ms"], "detect": detect,
             "n_super_hosts": int(len(hosts)) if hosts is not None else None,
-            "roofline": roofline, **({"roofline_hbm": roofline_hbm} if roofline_hbm else {}),
-            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e,
+            "roofline": roofline, "gpu_launches": int(nlaunch), "clocks": clk.summary(), "e2e": e2e,
+            "access_peaks": {k: v / 1e9 for k, v in peaks_acc.items()},
             "baseline_note": "paper publishes no pairs/s (BASELINE.md); its restore time is <11 ms on a Titan Xp"}
+    if args.workload == "C2" and args.seed == 1 and world == 1:
+        line["parity"] = golden_check(hosts)
+    if e2e is None:
+        line["e2e_note"] = "C4 keeps no host copy of its 16 GB window" if not keep_host else "disabled (--no-e2e)"
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w)
+        line["cpu_baseline"] = cpu_baseline(host_blocks)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

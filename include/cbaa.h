@@ -58,6 +58,10 @@ extern "C" {
 #define CBAA_THETA_INVERTED 1 /* θ_bn = g(1−ε)e^{−θ/g}, Theorem 2 inverted (Q15)           */
 
 /* How the update kernel sets a bit; the resulting cube is identical (bits only go 0 -> 1). */
+/* Union-column threshold of Alg. 3 (Q20). */
+#define CBAA_UNION_SAME 0     /* reuse the per-CS θ_bn of Alg. 2 for the union column (paper as written)  */
+#define CBAA_UNION_THM2 1     /* θ_uc = g(1−ε)e^{−θ/g}: accept iff the Thm. 2 estimate of UC is ≥ θ         */
+
 #define CBAA_UPDATE_TEST_SET 0  /* L1-cached load of the word; RED.OR only if the bit is still 0           */
 #define CBAA_UPDATE_RED 1       /* unconditional RED.OR per bit: the paper's write-only update   */
 #define CBAA_UPDATE_BINNED 2    /* pairs binned by (CS, row group) and applied in shared memory (large n) */
@@ -100,7 +104,10 @@ typedef struct {
   uint32_t bin_min_pairs;              /* CBAA_UPDATE_BINNED: calls with fewer pairs take the direct      */
                                        /* kernel (0 = auto: max(2^20, cube words / 4), and cubes up to    */
                                        /* 0.6 of L2 always direct)                                         */
-  uint32_t reserved[2];
+  int32_t union_threshold;             /* Alg. 3 threshold (Q20): CBAA_UNION_SAME (default, θ_bn of Alg. 2 as */
+                                       /* written at P:309) | CBAA_UNION_THM2 (θ_uc = g(1−ε)e^{−θ/g}: Thm. 2  */
+                                       /* solved for Z, so a host is output iff its estimate ≥ θ)    */
+  uint32_t reserved;
 } cbaa_config;
 
 /* One restored super host (Alg. 3 output). */
@@ -124,7 +131,9 @@ typedef struct {
   uint64_t candidates;    /* tuples passing the CP check (Alg. 3)                 */
   uint64_t hits;          /* candidates accepted by the union-column test           */
   int32_t overflow;       /* 1: tuples > tuple_cap, CS skipped                      */
-  int32_t _pad;
+  uint32_t zmax_uc;       /* ⌊θ_uc⌋ clamped to [0, g]: Alg. 3 accepts Z_uc ≤ zmax_uc (= zmax   */
+                          /* unless union_threshold = CBAA_UNION_THM2)                         */
+  double theta_uc;        /* union-column threshold of Alg. 3 (= theta_bn by default, Q20)   */
 } cbaa_cs_stats;
 
 /* ---------------------------------------------------------------- host only

@@ -21,6 +21,7 @@ MAX_RA, MAX_VA, MAX_ARRAYS, MAX_PREFIXES = 8, 8, 16, 16
 OK = 0
 E_CONFIG, E_ARG, E_CUDA, E_MISMATCH, E_CAPACITY, E_TUPLE_CAP, E_NOMEM = -1, -2, -3, -4, -5, -6, -7
 THETA_PAPER, THETA_INVERTED = 0, 1
+UNION_SAME, UNION_THM2 = 0, 1
 DIR_NORMALIZED, DIR_INNER_PREFIX = 0, 1
 UPDATE_TEST_SET, UPDATE_RED, UPDATE_BINNED = 0, 1, 2
 SKETCH_REPLACE, SKETCH_MERGE = 0, 1
@@ -37,7 +38,7 @@ class Config(C.Structure):
         ("n_prefixes", C.c_uint32), ("inner_prefix", C.c_uint32 * MAX_PREFIXES),
         ("inner_mask", C.c_uint32 * MAX_PREFIXES), ("update_passes", C.c_uint32), ("hit_capacity", C.c_uint32),
         ("update_mode", C.c_uint32), ("join_capacity", C.c_uint32), ("detect_overlap", C.c_uint32),
-        ("bin_min_pairs", C.c_uint32), ("reserved", C.c_uint32 * 2),
+        ("bin_min_pairs", C.c_uint32), ("union_threshold", C.c_int32), ("reserved", C.c_uint32),
     ]
 
     def to_dict(self) -> dict:
@@ -46,6 +47,7 @@ class Config(C.Structure):
                     clbs=list(self.clbs[: self.num_ra]), mangle_a=self.mangle_a, mangle_b=self.mangle_b,
                     bv_seed=self.bv_seed, va_seeds=list(self.va_seeds[: self.num_va]),
                     theta_formula=self.theta_formula, tuple_cap=self.tuple_cap, direction=self.direction,
+                    union_threshold=self.union_threshold,
                     prefixes=[(self.inner_prefix[k], self.inner_mask[k]) for k in range(self.n_prefixes)])
 
 
@@ -57,7 +59,8 @@ class Host(C.Structure):
 class CsStats(C.Structure):
     _fields_ = [("ztot", C.c_uint64), ("eta", C.c_double), ("eps", C.c_double), ("theta_bn", C.c_double),
                 ("zmax", C.c_uint32), ("n_hot", C.c_uint32 * MAX_RA), ("tuples", C.c_uint64),
-                ("candidates", C.c_uint64), ("hits", C.c_uint64), ("overflow", C.c_int32), ("_pad", C.c_int32)]
+                ("candidates", C.c_uint64), ("hits", C.c_uint64), ("overflow", C.c_int32), ("zmax_uc", C.c_uint32),
+                ("theta_uc", C.c_double)]
 
 
 HOST_DTYPE = np.dtype([("ip", "<u4"), ("cs", "<u4"), ("lp", "<u4"), ("z", "<u4"), ("estimate", "<f8")])
@@ -158,6 +161,7 @@ def config_from_dict(p: dict) -> Config:
     c.join_capacity = p.get("join_capacity", 0)
     c.detect_overlap = p.get("detect_overlap", 0)
     c.bin_min_pairs = p.get("bin_min_pairs", 0)
+    c.union_threshold = p.get("union_threshold", UNION_SAME)
     return c
 
 
@@ -314,7 +318,8 @@ class Cbaa:
         hosts = out[: min(n.value, cap)].copy()
         if stats is None:
             return hosts, None, rc
-        sd = [dict(ztot=s.ztot, eta=s.eta, eps=s.eps, theta_bn=s.theta_bn, zmax=s.zmax,
+        sd = [dict(ztot=s.ztot, eta=s.eta, eps=s.eps, theta_bn=s.theta_bn, zmax=s.zmax, zmax_uc=s.zmax_uc,
+                   theta_uc=s.theta_uc,
                    n_hot=list(s.n_hot[: self.cfg.num_ra]), tuples=s.tuples, candidates=s.candidates, hits=s.hits,
                    overflow=s.overflow) for s in stats]
         return hosts, sd, rc

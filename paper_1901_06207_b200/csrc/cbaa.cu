@@ -21,14 +21,14 @@
 
 using namespace cbaa;
 
-struct DetectKey {
-  uint32_t cs_lo = 0, cs_hi = 0, theta = 0;
+struct DetectKey {   // what a captured detect graph depends on (θ is not part of it: see hot_node)
+  uint32_t cs_lo = 0, cs_hi = 0;
   int record = 0;
   const void* cand = nullptr;
   const void* h_res = nullptr;
   int join = 0;
   bool operator==(const DetectKey& o) const {
-    return cs_lo == o.cs_lo && cs_hi == o.cs_hi && theta == o.theta && record == o.record && cand == o.cand &&
+    return cs_lo == o.cs_lo && cs_hi == o.cs_hi && record == o.record && cand == o.cand &&
            h_res == o.h_res && join == o.join;
   }
 };
@@ -68,8 +68,12 @@ struct cbaa_handle {
   int upd_blocks = 0;
   // detect graph (captured on cap_stream, launched on the caller's stream)
   cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;          // kept alive: hot_node belongs to it
   cudaGraphExec_t graph_exec = nullptr;
   DetectKey graph_key{};
+  cudaGraphNode_t hot_node = nullptr;   // the k_hot node: θ is set per detect by a kernel-node parameter update
+  cudaKernelNodeParams hot_params{};
+  uint32_t graph_theta = 0;             // θ currently in the instantiated graph
   int graph_kernels = 0;
   int use_join = 0;          // |RA| = 3 and not forced Cartesian
   // binned update (CBAA_UPDATE_BINNED, binned.cuh)
@@ -168,6 +172,8 @@ int validate(const cbaa_config* c, std::string* why) {
   }
   if (c->theta_formula != CBAA_THETA_PAPER && c->theta_formula != CBAA_THETA_INVERTED)
     return bad("theta_formula must be CBAA_THETA_PAPER or CBAA_THETA_INVERTED");
+  if (c->union_threshold != CBAA_UNION_SAME && c->union_threshold != CBAA_UNION_THM2)
+    return bad("union_threshold must be CBAA_UNION_SAME or CBAA_UNION_THM2 (Q20)");
   if (c->direction != CBAA_DIR_NORMALIZED && c->direction != CBAA_DIR_INNER_PREFIX)
     return bad("direction must be CBAA_DIR_NORMALIZED or CBAA_DIR_INNER_PREFIX");
   if (c->n_prefixes > CBAA_MAX_PREFIXES) return bad("at most 16 inner prefixes");
@@ -234,6 +240,7 @@ Geo derive(const cbaa_config& c) {
   for (uint32_t j = 0; j < c.num_va; ++j) G.va_seeds[j] = c.va_seeds[j];
   G.direction = c.direction;
   G.theta_formula = c.theta_formula;
+  G.union_threshold = c.union_threshold;
   G.n_prefix = c.n_prefixes;
   for (uint32_t k = 0; k < c.n_prefixes; ++k) {
     G.prefix[k] = c.inner_prefix[k] & c.inner_mask[k];
@@ -764,6 +771,7 @@ void cbaa_destroy(cbaa_handle* h) {
   }
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
 }
@@ -951,12 +959,17 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   // of the CS records and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured
   // once per (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
   const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
-  const DetectKey key{cs_lo, cs_hi, theta, h->record, (const void*)D.cand, (const void*)h->h_res, h->use_join};
+  const DetectKey key{cs_lo, cs_hi, h->record, (const void*)D.cand, (const void*)h->h_res, h->use_join};
   if (!h->graph_exec || !(h->graph_key == key)) {
     if (h->graph_exec) {
       cudaGraphExecDestroy(h->graph_exec);
       h->graph_exec = nullptr;
     }
+    if (h->graph) {
+      cudaGraphDestroy(h->graph);
+      h->graph = nullptr;
+    }
+    h->hot_node = nullptr;
     if (!h->cap_stream) CK(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     cudaStream_t c = h->cap_stream;
     CK(h, cudaStreamBeginCapture(c, cudaStreamCaptureModeThreadLocal));
@@ -996,11 +1009,43 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     }
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaStreamEndCapture(detect)");
     e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
+    }
+    h->graph = graph;
+    // find the k_hot node: a later θ only rewrites that node's parameters in the executable graph
+    size_t nn = 0;
+    CK(h, cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(h, cudaGraphGetNodes(graph, nodes.data(), &nn));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      CK(h, cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      CK(h, cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == (void*)k_hot) {
+        h->hot_node = nd;
+        h->hot_params = kp;
+      }
+    }
+    if (!h->hot_node) return fail(h, CBAA_E_CUDA, "detect graph: k_hot node not found");
+    h->graph_theta = theta;
     h->graph_key = key;
     h->graph_kernels = (join ? 4 : 3) + (h->cfg.detect_overlap ? 0 : 1);
     h->launches -= h->graph_kernels;   // counted at capture; counted again per graph launch below
+  }
+  if (h->graph_theta != theta) {   // same graph, new θ: k_hot(G, D, cs_lo, n_range, theta, join)
+    void* args[6];
+    for (int i = 0; i < 6; ++i) args[i] = h->hot_params.kernelParams[i];
+    uint32_t th = theta;
+    args[4] = &th;
+    cudaKernelNodeParams kp = h->hot_params;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    CK(h, cudaGraphExecKernelNodeSetParams(h->graph_exec, h->hot_node, &kp));
+    h->graph_theta = theta;
   }
   CK(h, cudaGraphLaunch(h->graph_exec, s));
   h->launches += h->graph_kernels;

@@ -24,7 +24,7 @@ struct Geo {
   uint32_t ra_cols;                    // Σ_{i<num_ra} c(i)
   uint32_t mangle_a, mangle_b, inv_a, bv_seed;
   uint32_t va_seeds[CBAA_MAX_VA];
-  int32_t direction, theta_formula;
+  int32_t direction, theta_formula, union_threshold;
   uint32_t n_prefix;
   uint32_t prefix[CBAA_MAX_PREFIXES], pmask[CBAA_MAX_PREFIXES];
   // inner-prefix classification by the top 16 address bits: bit t of full_bits set ⇔ every address with

@@ -325,13 +325,21 @@ __device__ void cs_math(const Geo& G, uint64_t ztot, uint32_t theta, cbaa_cs_sta
   double tbn = G.theta_formula == CBAA_THETA_PAPER ? g * (1.0 + eps) * exp(-(double)theta / g) - g * eps
                                                    : g * (1.0 - eps) * exp(-(double)theta / g);
   if (tbn < 0.0) tbn = 0.0;
-  double f = floor(tbn);
-  uint32_t zmax = f < 0.0 ? 0u : (f > g ? G.g : (uint32_t)f);
+  // Alg. 3's union-column threshold (Q20): θ_bn as written, or θ_uc = g(1−ε)e^{−θ/g}, the Thm. 2
+  // estimate solved for Z so that a candidate is accepted iff its estimate reaches θ (Def. 1)
+  double tuc = G.union_threshold == CBAA_UNION_THM2 ? g * (1.0 - eps) * exp(-(double)theta / g) : tbn;
+  if (tuc < 0.0) tuc = 0.0;
+  auto zfloor = [&](double t) {
+    const double f = floor(t);
+    return f < 0.0 ? 0u : (f > g ? G.g : (uint32_t)f);
+  };
   rec->ztot = ztot;
   rec->eta = eta;
   rec->eps = eps;
   rec->theta_bn = tbn;
-  rec->zmax = zmax;
+  rec->zmax = zfloor(tbn);
+  rec->theta_uc = tuc;
+  rec->zmax_uc = zfloor(tuc);
 }
 
 struct DetectScratch {
@@ -545,6 +553,8 @@ __global__ void __launch_bounds__(kDetThreads) k_hot(const __grid_constant__ Geo
       rec->eps = st.eps;
       rec->theta_bn = st.theta_bn;
       rec->zmax = st.zmax;
+      rec->theta_uc = st.theta_uc;
+      rec->zmax_uc = st.zmax_uc;
       rec->candidates = 0;   // accumulated by the Alg. 3 kernels, which run after this grid
       rec->hits = 0;
     }
@@ -664,7 +674,7 @@ __device__ __forceinline__ void union_check(const Geo& G, const uint32_t* __rest
       unsigned long long k = atomicAdd(D.n_cand, 1ull);
       if (k < D.cand_cap) D.cand[k] = ((unsigned long long)cs << 32) | lp;
     }
-    if (z <= rec->zmax) {   // reject iff zero bits > θ_bn (Q16)
+    if (z <= rec->zmax_uc) {   // reject iff zero bits > θ_bn (Q16), or > θ_uc (Q20 option)
       atomicAdd(reinterpret_cast<unsigned long long*>(&rec->hits), 1ull);
       unsigned long long k = atomicAdd(D.n_hits, 1ull);
       if (k < D.hit_cap) {

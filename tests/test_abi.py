@@ -47,8 +47,9 @@ int main(void) {
   printf("cbaa_host size %zu\n", sizeof(cbaa_host));
   F(cbaa_config, cbn) F(cbaa_config, clbs) F(cbaa_config, mangle_a) F(cbaa_config, va_seeds)
   F(cbaa_config, theta_formula) F(cbaa_config, tuple_cap) F(cbaa_config, n_prefixes) F(cbaa_config, inner_mask)
-  F(cbaa_config, update_passes) F(cbaa_config, hit_capacity)
+  F(cbaa_config, update_passes) F(cbaa_config, hit_capacity) F(cbaa_config, union_threshold)
   F(cbaa_cs_stats, zmax) F(cbaa_cs_stats, n_hot) F(cbaa_cs_stats, tuples) F(cbaa_cs_stats, overflow)
+  F(cbaa_cs_stats, zmax_uc) F(cbaa_cs_stats, theta_uc)
   F(cbaa_host, z) F(cbaa_host, estimate)
   return 0;
 }

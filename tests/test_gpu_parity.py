@@ -33,9 +33,9 @@ def gpu_cube(cb):
 def assert_stats_equal(gs, os_):
     assert len(gs) == len(os_)
     for cs, (a, b) in enumerate(zip(gs, os_)):
-        for k in ("ztot", "zmax", "n_hot", "tuples", "candidates", "hits", "overflow"):
+        for k in ("ztot", "zmax", "zmax_uc", "n_hot", "tuples", "candidates", "hits", "overflow"):
             assert a[k] == b[k], (cs, k, a[k], b[k])
-        for k in ("eta", "eps", "theta_bn"):
+        for k in ("eta", "eps", "theta_bn", "theta_uc"):
             if np.isinf(b[k]) or b[k] == 0:
                 assert a[k] == b[k], (cs, k)
             else:

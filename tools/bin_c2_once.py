@@ -1,4 +1,5 @@
-"""One binned C2 update (for ncu captures)."""
+"""Three binned C2 updates then one detect, for ncu captures (tools/gpu_round.sh ncu: -k k_bin_*|detect
+kernels -s 10 -c 9 = the third update's 5 kernels + the detect's 4)."""
 import sys
 
 import numpy as np
@@ -13,10 +14,9 @@ w = W.generate(W.C2, 1, with_raw=False)
 s = torch.from_numpy(w.src.view(np.int32)).cuda()
 d = torch.from_numpy(w.dst.view(np.int32)).cuda()
 cb = Cbaa(config_from_dict(dict(O.default_params(), update_mode=int(sys.argv[1]) if len(sys.argv) > 1 else 2)), 0)
-for _ in range(2):
+for _ in range(3):
     cb.reset()
     cb.update(s, d)
+hosts, _, _ = cb.detect(1024)
 torch.cuda.synchronize()
-if len(sys.argv) > 2:   # occupancy report of the binned kernels
-    import ctypes
-    print("max active scatter CTAs/SM reported via ncu launch__occupancy_limit_shared_mem")
+print(len(hosts), "hosts")

@@ -17,6 +17,10 @@ KEYS = {
     "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1.0),
     "l1_hit_pct": ("l1tex__t_sector_hit_rate.pct", 1.0),
     "red_sectors_to_l2": ("lts__t_sectors_srcunit_tex_op_red.sum", 1.0),
+    "red_requests_to_l2": ("lts__t_requests_srcunit_tex_op_red.sum", 1.0),
+    "atom_requests_to_l2": ("lts__t_requests_srcunit_tex_op_atom.sum", 1.0),
+    "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1.0),
+    "smem_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1.0),
     "global_load_sectors": ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 1.0),
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
