@@ -258,6 +258,23 @@ def update(p, src, dst, cube: np.ndarray | None = None):
     return cube, skipped.value
 
 
+def update_parallel(p, src, dst, threads: int | None = None):
+    """Alg. 1 over a stream on `threads` host threads: each updates a private cube from a contiguous block,
+    then the cubes are OR-merged (mergeCubes).  Equal to update() by the shard-OR invariant (S:105,
+    pinned in tests/test_oracle_pins.py); only the wall time differs.  Returns the cube."""
+    from concurrent.futures import ThreadPoolExecutor
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    threads = max(1, min(threads or os.cpu_count() or 1, max(1, src.size // 65536)))
+    cuts = [src.size * t // threads for t in range(threads + 1)]
+    with ThreadPoolExecutor(threads) as ex:   # ctypes drops the GIL inside orc_update
+        cubes = list(ex.map(lambda t: update(p, src[cuts[t]:cuts[t + 1]], dst[cuts[t]:cuts[t + 1]])[0],
+                            range(threads)))
+    for c in cubes[1:]:
+        merge(cubes[0], c)
+    return cubes[0]
+
+
 def merge(dst: np.ndarray, src: np.ndarray) -> np.ndarray:
     assert dst.size == src.size
     lib().orc_merge(_ptr(dst), _ptr(src), dst.size)

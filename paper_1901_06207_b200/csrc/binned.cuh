@@ -268,20 +268,24 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
   const uint32_t prm = kPaper ? 15u : pin(G.rmask), pr = kPaper ? 4u : pin(G.r);
   const uint32_t pbl = kPaper ? 8u : pin(B.bpc_log2), pes = kPaper ? 4u : pin(B.s);
   const uint32_t psm = kPaper ? 15u : pin((1u << B.s) - 1u), toff_sa = pin(smem_addr(toff));
+  // all kBinPPT pairs of the thread are loaded before any is hashed (one DRAM latency per tile), then
+  // each pair's registers are reused for its key (bin, rank in the tile) and entry.  (Issuing the next
+  // tile's loads right after the staging pass measured slower: profiles/r02_scatter_ab.md)
+  uint32_t key[kBinPPT], ent[kBinPPT];
+  auto load_whole = [&](uint64_t t) {
+#pragma unroll
+    for (int q = 0; q < kBinPPT / 4; ++q) {
+      const uint64_t k = t + 4ull * ((uint64_t)q * kBinThreads + tid);
+      const uint4 a = ld_stream4(src + k), b = ld_stream4(dst + k);
+      key[4 * q] = a.x, key[4 * q + 1] = a.y, key[4 * q + 2] = a.z, key[4 * q + 3] = a.w;
+      ent[4 * q] = b.x, ent[4 * q + 1] = b.y, ent[4 * q + 2] = b.z, ent[4 * q + 3] = b.w;
+    }
+  };
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
-    // all kBinPPT pairs of the thread are loaded before any is hashed (one DRAM latency per tile), then
-    // each pair's registers are reused for its key (bin, rank in the tile) and entry
-    uint32_t key[kBinPPT], ent[kBinPPT];
     if (!PREFIX && vec && t0 + kBinTile <= c1) {
       // whole tile, normalised input: no per-pair checks; parameters pinned in registers
-#pragma unroll
-      for (int q = 0; q < kBinPPT / 4; ++q) {
-        const uint64_t k = t0 + 4ull * ((uint64_t)q * kBinThreads + tid);
-        const uint4 a = ld_stream4(src + k), b = ld_stream4(dst + k);
-        key[4 * q] = a.x, key[4 * q + 1] = a.y, key[4 * q + 2] = a.z, key[4 * q + 3] = a.w;
-        ent[4 * q] = b.x, ent[4 * q + 1] = b.y, ent[4 * q + 2] = b.z, ent[4 * q + 3] = b.w;
-      }
+      load_whole(t0);
 #pragma unroll
       for (int i = 0; i < kBinPPT; ++i) {
         const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;           // P:175, Q2
@@ -304,11 +308,14 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
       }
     }
     __syncthreads();
-    // Warp w owns bins [w·wchunk, (w+1)·wchunk), lane l every 32nd of them (conflict-free).  First the
-    // runs are reserved at the global cursors (a warp's 32 atomics hit one line of the cursors; 16 in
-    // flight per thread).  Then each bin gets its run in the staging array: the staging order only has
-    // to keep a bin's entries together, so it is thread-major — thread t's bins follow each other — and
-    // one scan of the per-thread totals places every run.
+    // Warp w owns bins [w·wchunk, (w+1)·wchunk): in row j (32 consecutive bins) lane l owns bin
+    // 32j + ((l + j) mod 32), so a warp touches 32 consecutive words per row (conflict-free, and its 32
+    // reservation atomics hit one line of the cursors; 16 in flight per thread).  Then each bin gets its
+    // run in the staging array: the staging order only has to keep a bin's entries together, so it is
+    // thread-major — thread t's bins follow each other — and one scan of the per-thread totals places
+    // every run.  The (l + j) rotation puts a thread's consecutive runs in different banks: the write-out's
+    // base[bin] loads of 32 consecutive staging positions (~16 runs of one thread) are then conflict-free
+    // instead of 16-way (lane-strided ownership without it: bins 32 apart, one bank).
     {
       const int lane = tid & 31, warp = tid >> 5;
       const uint32_t w0 = warp * wchunk;
@@ -317,17 +324,19 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
         uint32_t x[16], r[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const uint32_t b = w0 + i0 + 32 * j + lane;
+          const uint32_t b = w0 + i0 + 32 * j + ((lane + j) & 31);
           x[j] = (i0 + 32 * j < wchunk && b < nbins) ? toff[b] : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = x[j] ? atomicAdd(cursor + (w0 + i0 + 32 * j + lane) * kCurStride, x[j]) : 0u;
+        for (int j = 0; j < 16; ++j)
+          r[j] = x[j] ? atomicAdd(cursor + (w0 + i0 + 32 * j + ((lane + j) & 31)) * kCurStride, x[j]) : 0u;
         bool over = false;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (x[j]) {
-            base[w0 + i0 + 32 * j + lane] = r[j];
-            over |= r[j] + x[j] > rend[w0 + i0 + 32 * j + lane];
+            const uint32_t b = w0 + i0 + 32 * j + ((lane + j) & 31);
+            base[b] = r[j];
+            over |= r[j] + x[j] > rend[b];
           }
           loc += x[j];
         }
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
       for (uint32_t i0 = 0; i0 < wchunk; i0 += 32 * 16) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const uint32_t b = w0 + i0 + 32 * j + lane;
+          const uint32_t b = w0 + i0 + 32 * j + ((lane + j) & 31);
           if (i0 + 32 * j < wchunk && b < nbins) {
             const uint32_t x = toff[b];
             toff[b] = run;
@@ -572,6 +581,247 @@ __device__ __forceinline__ void reds_or(uint32_t a, uint32_t bit) {
 __device__ __forceinline__ void reds_or_if_clear(uint32_t a, uint32_t bit, uint32_t v) {
   asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %2, 0;\n @p red.shared.or.b32 [%0], %1;\n}" ::"r"(a), "r"(bit),
                "r"(v & bit));
+}
+
+// ---------------------------------------------------------------- wide entries (the paper configuration)
+// With r = 4 a 32-bit entry holds LP (28 bits) and only s = 4 row bits, so a word group (32 rows) is
+// split over two bins and an 8192-pair tile meets 4096 bins: runs of ~2 entries, and the write-out
+// of a warp touches ~16 lines per store (profiles/r02_scatter_ab.md: that write-out is 0.24 of the
+// scatter's 0.66 ms; with perfectly coalesced stores the scatter takes 0.46 ms).  Wide entries are
+// 64-bit — LP << 6 | row mod 64 — so a bin is (cs, row >> 6), two word groups: 1024 bins, runs of ~8
+// entries (64 B), 4× fewer reservation atomics, and the bin rides in the staged entry's top bits
+// (no separate bin array).  The apply gives each bin one CTA with a 128 KiB image of its two word groups.
+// DRAM: 8 instead of 4 B written and read back per pair.
+constexpr int kWBins = 1024;                   // 2^4 CSs × 4096 / 64 rows
+constexpr int kWRankBits = 14;
+#ifndef CBAA_WAPPLY_THREADS
+#define CBAA_WAPPLY_THREADS 1024
+#endif
+constexpr int kWApplyThreads = CBAA_WAPPLY_THREADS;
+constexpr uint64_t kWEntMask = (1ull << 48) - 1;   // staged entry: bin << 48 | LP << 6 | row mod 64
+constexpr size_t kWScatterSmem = (size_t)kBinTile * 8 + (3 * kWBins + 1) * 4;   // 76 KiB: two CTAs per SM
+constexpr size_t kWApplySmem = 2 * 16384 * 4;                                   // two word groups, 128 KiB
+
+__global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(const __grid_constant__ Geo G,
+                                                             const uint32_t* __restrict__ src,
+                                                             const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
+                                                             int vec, uint32_t* __restrict__ cursor,
+                                                             uint64_t* __restrict__ entries,
+                                                             const uint32_t* __restrict__ start,
+                                                             uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e) {
+  constexpr uint32_t nbins = kWBins;
+  constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread
+  constexpr uint32_t wchunk = kPerLane * 32;              // 128 bins per warp
+  extern __shared__ __align__(16) uint64_t smw[];
+  uint64_t* stage = smw;                                  // [kBinTile] bin << 48 | entry, sorted by bin
+  uint32_t* base = reinterpret_cast<uint32_t*>(stage + kBinTile);   // [nbins] this tile's slot base
+  uint32_t* toff = base + nbins;                          // [nbins + 1] tile counts → exclusive offsets
+  uint32_t* rend = toff + nbins + 1;                      // [nbins] region ends start[b + 1]
+  __shared__ uint32_t s_w[kBinThreads / 32];
+  __shared__ int s_ovf;
+  const uint32_t tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (uint32_t b = tid; b < nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
+  if (tid == 0) s_ovf = 0;
+  const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
+  const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), toff_sa = pin(smem_addr(toff));
+  const uint32_t w0 = warp * wchunk;
+  __syncthreads();
+  for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
+    // key = (row mod 64) << 24 | bin << 14 | rank in the tile; ent = LP
+    uint32_t key[kBinPPT], ent[kBinPPT];
+    const bool whole = vec && t0 + kBinTile <= c1;
+    if (whole) {
+#pragma unroll
+      for (int q = 0; q < kBinPPT / 4; ++q) {
+        const uint64_t k = t0 + 4ull * ((uint64_t)q * kBinThreads + tid);
+        const uint4 a = ld_stream4(src + k), b = ld_stream4(dst + k);
+        key[4 * q] = a.x, key[4 * q + 1] = a.y, key[4 * q + 2] = a.z, key[4 * q + 3] = a.w;
+        ent[4 * q] = b.x, ent[4 * q + 1] = b.y, ent[4 * q + 2] = b.z, ent[4 * q + 3] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kBinPPT; ++i) {
+        const uint64_t k = t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3);
+        key[i] = k < c1 ? __ldcs(src + k) : 0u;
+        ent[i] = k < c1 ? __ldcs(dst + k) : 0u;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kBinPPT; ++i) {
+      const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;           // P:175, Q2
+      const uint32_t row = mix32(mo ^ pbv) & 4095u;                         // P:230 (g = 4096)
+      const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                  // (cs, row >> 6), r = 4
+      ent[i] = mi >> 4;                                                     // LP
+      const bool ok = whole || t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3) < c1;
+      key[i] = ok ? ((row & 63u) << 24) | (bin << kWRankBits) | atoms_inc(toff_sa + 4u * bin) : 0xffffffffu;
+    }
+    __syncthreads();
+    // per-bin reservation and offsets (rotated lane ownership as in k_bin_scatter)
+    {
+      uint32_t x[kPerLane], r[kPerLane], loc = 0;
+      bool over = false;
+#pragma unroll
+      for (int j = 0; j < (int)kPerLane; ++j) x[j] = toff[w0 + 32 * j + ((lane + j) & 31)];
+#pragma unroll
+      for (int j = 0; j < (int)kPerLane; ++j)
+        r[j] = x[j] ? atomicAdd(cursor + (w0 + 32 * j + ((lane + j) & 31)) * kCurStride, x[j]) : 0u;
+#pragma unroll
+      for (int j = 0; j < (int)kPerLane; ++j) {
+        const uint32_t b = w0 + 32 * j + ((lane + j) & 31);
+        if (x[j]) {
+          base[b] = r[j];
+          over |= r[j] + x[j] > rend[b];
+        }
+        loc += x[j];
+      }
+      if (over) s_ovf = 1;
+      uint32_t incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_w[warp] = incl;
+      __syncthreads();
+      uint32_t run = incl - loc, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kBinThreads / 32; ++w) {
+        run += w < warp ? s_w[w] : 0u;
+        tot += s_w[w];
+      }
+#pragma unroll
+      for (int j = 0; j < (int)kPerLane; ++j) {
+        const uint32_t b = w0 + 32 * j + ((lane + j) & 31);
+        toff[b] = run;
+        if (x[j]) base[b] -= run;   // base[b] + p is the slot of staging position p
+        run += x[j];
+      }
+      if (tid == 0) toff[nbins] = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kBinPPT; ++i) {
+      if (key[i] == 0xffffffffu) continue;
+      const uint32_t bin = (key[i] >> kWRankBits) & (nbins - 1u);
+      const uint32_t pos = toff[bin] + (key[i] & ((1u << kWRankBits) - 1u));
+      stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | (key[i] >> 24);
+    }
+    __syncthreads();
+    const uint32_t total = toff[nbins];
+    if (!s_ovf) {
+#pragma unroll 4
+      for (uint32_t p = tid; p < total; p += kBinThreads) {
+        const uint64_t v = stage[p];
+        entries[base[(uint32_t)(v >> 48)] + p] = v & kWEntMask;
+      }
+    } else {   // past a region's end (a sampled capacity fell short): to the overflow log, bin included
+      for (uint32_t p = tid; p < total; p += kBinThreads) {
+        const uint64_t v = stage[p];
+        const uint32_t bin = (uint32_t)(v >> 48), g = base[bin] + p;
+        if (g < rend[bin]) entries[g] = v & kWEntMask;
+        else log_e[atomicAdd(log_n, 1u)] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < (int)kPerLane; ++j) toff[w0 + 32 * j + lane] = 0;
+    if (tid == 0) s_ovf = 0;
+    __syncthreads();
+  }
+}
+
+// The paper configuration's column extraction: RA(i) = bits [clbs(i), clbs(i) + 12) of the 28-bit LP
+// (MSB-first, wrapping; clbs [0, 10, 20]: shifts 44/34/24 of the doubled LP), VA = mix32(LP ⊕ seed)
+// (P:235); image offset of array a = 4096·a words.
+__device__ __forceinline__ void paper_cols(uint32_t lp, uint32_t vseed, uint32_t c[4]) {
+  const uint64_t dbl = ((uint64_t)lp << 28) | lp;
+  c[0] = (uint32_t)(dbl >> 44) & 4095u;
+  c[1] = (uint32_t)(dbl >> 34) & 4095u;
+  c[2] = (uint32_t)(dbl >> 24) & 4095u;
+  c[3] = mix32(lp ^ vseed) & 4095u;
+}
+
+// Apply of the wide entries: one CTA per bin (cs, row >> 6) = two word groups, image sub[h][16384]
+// (h = bit 5 of the row); test-and-set in shared memory, then one RED per non-zero word.
+__global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_w(const __grid_constant__ Geo G,
+                                                                  const uint32_t* __restrict__ start,
+                                                                  const uint32_t* __restrict__ end,
+                                                                  const uint64_t* __restrict__ entries,
+                                                                  uint32_t* __restrict__ cube) {
+  extern __shared__ uint32_t sub[];
+  constexpr uint32_t kCols = 16384;   // Σc(i) words of one word group (paper configuration)
+  const uint32_t sbase = pin(smem_addr(sub));
+  const uint32_t b = blockIdx.x, cs = b >> 6, wq = b & 63u;
+  for (uint32_t i = threadIdx.x; i < 2 * kCols / 4; i += kWApplyThreads)
+    reinterpret_cast<uint4*>(sub)[i] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t vseed = pin(G.va_seeds[0]);
+  __syncthreads();
+  const uint32_t P0 = start[b], E0 = min(end[b * kCurStride], start[b + 1]);
+  const uint64_t* __restrict__ ent = entries + P0;
+  const uint32_t len = E0 - P0;
+  auto set_bits = [&](uint64_t e) {
+    const uint32_t lp = (uint32_t)(e >> 6), r6 = (uint32_t)e & 63u;
+    const uint32_t bit = 1u << (r6 & 31u), hb = sbase + (r6 >> 5) * (4u * kCols);
+    uint32_t c[4], adr[4], v[4];
+    paper_cols(lp, vseed, c);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      adr[a] = hb + 16384u * (uint32_t)a + 4u * c[a];
+      v[a] = lds(adr[a]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) reds_or_if_clear(adr[a], bit, v[a]);
+  };
+  constexpr uint32_t kStep = kApplyUnroll * kWApplyThreads;
+  uint64_t e[kApplyUnroll];
+  uint32_t p = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kWApplyThreads < len ? __ldcs(ent + p + u * kWApplyThreads) : 0ull;
+  while (p < len) {
+    const uint32_t pn = p + kStep;
+    uint64_t en[kApplyUnroll];
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      en[u] = pn + u * kWApplyThreads < len ? __ldcs(ent + pn + u * kWApplyThreads) : 0ull;
+    if (p + (kApplyUnroll - 1) * kWApplyThreads < len) {
+#pragma unroll
+      for (int u = 0; u < kApplyUnroll; ++u) set_bits(e[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kApplyUnroll; ++u)
+        if (p + u * kWApplyThreads < len) set_bits(e[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
+    p = pn;
+  }
+  __syncthreads();
+  // image word h·16384 + i = word (2·wq + h) of column i of CS cs
+  uint32_t* cw = cube + (uint64_t)cs * G.cs_words + 2u * wq;
+  for (uint32_t i = threadIdx.x; i < 2 * kCols; i += kWApplyThreads) {
+    const uint32_t v = sub[i];
+    if (v) red_or(cw + (uint64_t)(i & (kCols - 1u)) * G.wpc + (i >> 14), v);
+  }
+}
+
+// Overflow log of the wide scatter: records bin << 48 | LP << 6 | row mod 64, applied with the direct
+// update's test-and-set.
+__global__ void k_bin_log_w(const __grid_constant__ Geo G, const uint32_t* __restrict__ log_n,
+                            const uint64_t* __restrict__ log_e, uint32_t* __restrict__ cube) {
+  const uint32_t nrec = *log_n;
+  const uint32_t vseed = G.va_seeds[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+    const uint64_t v = log_e[i];
+    const uint32_t bin = (uint32_t)(v >> 48), cs = bin >> 6, row = ((bin & 63u) << 6) | ((uint32_t)v & 63u);
+    const uint32_t lp = (uint32_t)(v >> 6) & ((1u << 28) - 1u), bit = 1u << (row & 31u);
+    uint32_t c[4];
+    paper_cols(lp, vseed, c);
+    for (uint32_t a = 0; a < 4; ++a) {
+      uint32_t* w = cube + (uint64_t)cs * G.cs_words + G.arr_off[a] + (uint64_t)c[a] * G.wpc + (row >> 5);
+      if (!(__ldca(w) & bit)) red_or(w, bit);
+    }
+  }
 }
 
 // Phase 4: one CTA per word group (cs, w): its bins' entries set bits in a shared-memory image of the

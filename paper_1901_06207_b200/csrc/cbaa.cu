@@ -86,6 +86,8 @@ struct cbaa_handle {
   uint32_t* bin_tab = nullptr;    // counts | start | cursor | log count
   void* bin_log = nullptr;        // k_bin_wc overflow log
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
+  int bin_wide = 0;               // the paper configuration: 64-bit entries, 1024 bins (k_bin_scatter_w, binned.cuh)
+  BinGeo BW{};                    // bin geometry of the wide path
   bool apply_paper = false;       // k_bin_apply<3, 1, 4, true>: the paper's default configuration
   uint32_t bin_sample_log2 = 9;   // regions sized from 8 pairs of every 2^L (0: exact count; CBAA_BIN_SAMPLE)
   uint64_t bin_sample_min = 1ull << 24;   // chunks with fewer pairs are counted exactly (CBAA_BIN_SAMPLE_MIN)
@@ -442,10 +444,11 @@ void t_end(cbaa_handle* h, int k, cudaStream_t s) {
 // Binned update (binned.cuh): count → starts → scatter → apply, in chunks of at most 2^28 pairs.
 int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t kChunk = h->bin_chunk;
-  const BinGeo& B = h->B;
+  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+  const bool wide = h->bin_wide && !prefix && !h->bin_wc;   // 64-bit entries, 1024 bins
+  const BinGeo& B = wide ? h->BW : h->B;
   // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
   const uint32_t slack = h->bin_wc ? 8u * (uint32_t)h->sms : 0u;
-  const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
   // sampled region sizing (k_bin_sample): normalised input, tile scatter, chunks of ≥ bin_sample_min pairs
   const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
   const uint64_t mx = std::min(n, kChunk);
@@ -462,15 +465,17 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     if (h->bin_ent) CK(h, cudaFree(h->bin_ent));
     h->bin_ent = nullptr;
     h->bin_cap = 0;
-    CK(h, cudaMalloc(&h->bin_ent, want * 4));
+    CK(h, cudaMalloc(&h->bin_ent, want * 8));   // 8 B per entry: either entry width fits
     if (h->bin_log) CK(h, cudaFree(h->bin_log));
     h->bin_log = nullptr;
-    CK(h, cudaMalloc(&h->bin_log, std::min(n, kChunk) * 6 + 16));   // overflow log: u32 entries | u16 bins
+    // overflow log: u32 entries | u16 bins, or u64 records (wide)
+    CK(h, cudaMalloc(&h->bin_log, std::min(n, kChunk) * 8 + 16));
     h->bin_cap = want;   // only once both buffers exist (a failed allocation is retried on the next call)
   }
   if (!h->bin_tab) {   // counts [nbins] | start [nbins + 1] | cursor [nbins · kCurStride] | log count
-    CK(h, cudaMalloc(&h->bin_tab, ((2ull + kCurStride) * B.nbins + 2) * 4));
-    CK(h, cudaMemsetAsync(h->bin_tab, 0, (uint64_t)B.nbins * 4, s));
+    const uint64_t nb = std::max(h->B.nbins, h->BW.nbins);   // one table serves both entry widths
+    CK(h, cudaMalloc(&h->bin_tab, ((2ull + kCurStride) * nb + 2) * 4));
+    CK(h, cudaMemsetAsync(h->bin_tab, 0, nb * 4, s));
   }
   uint32_t* counts = h->bin_tab;
   uint32_t* start = counts + B.nbins;
@@ -507,7 +512,11 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     t_end(h, tk, s);
     if ((rc = launch_check(h, "k_bin_starts"))) return rc;
     tk = t_begin(h, 2, s);
-    if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
+    if (wide) {
+      k_bin_scatter_w<<<B.nblk, kBinThreads, kWScatterSmem, s>>>(h->G, a, b, m, per, vec, cursor,
+                                                                 (uint64_t*)h->bin_ent, start, log_n,
+                                                                 (uint64_t*)h->bin_log);
+    } else if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
       const uint32_t nw = (uint32_t)h->sms;
       const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
       if (prefix)
@@ -531,7 +540,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
     tk = t_begin(h, 3, s);
-    if (h->apply_paper)
+    if (wide)
+      k_bin_apply_w<<<B.nbins, kWApplyThreads, kWApplySmem, s>>>(h->G, start, cursor, (const uint64_t*)h->bin_ent,
+                                                                 h->cube);
+    else if (h->apply_paper)
       k_bin_apply<3, 1, 4, true><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
       k_bin_apply<3, 1, 4><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
@@ -540,7 +552,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     else
       k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
-    if (h->bin_wc || sl) {   // the scatter's overflow log (usually empty: the kernel exits at once)
+    if (wide && sl) {
+      k_bin_log_w<<<h->sms, 256, 0, s>>>(h->G, log_n, (const uint64_t*)h->bin_log, h->cube);
+      if ((rc = launch_check(h, "k_bin_log_w"))) return rc;
+    } else if (h->bin_wc || sl) {   // the scatter's overflow log (usually empty: the kernel exits at once)
       k_bin_log<<<h->sms, 256, 0, s>>>(h->G, B, log_n, log_e, log_b, h->cube);
       if ((rc = launch_check(h, "k_bin_log"))) return rc;
     }
@@ -733,6 +748,18 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
         bool pp = g.num_ra == 3 && g.num_va == 1 && B.s == 4 && g.sh[0] == 44 && g.sh[1] == 34 && g.sh[2] == 24;
         for (uint32_t a = 0; a < 4 && pp; ++a) pp = g.colmask[a] == 4095u && (g.arr_off[a] >> g.wpc_log2) == 4096u * a;
         h->apply_paper = pp;
+        // wide entries for the paper configuration (r = 4, g = 4096): CBAA_BIN_WIDE=0 keeps 32-bit entries
+        const char* bw = std::getenv("CBAA_BIN_WIDE");
+        h->bin_wide = pp && g.r == 4 && g.g == 4096 && !(bw && bw[0] == '0');
+        BinGeo& W = h->BW;
+        W.s = 6;
+        W.bpc_log2 = 6;
+        W.nbins = h->G.n_cs << 6;
+        W.nblk = B.nblk;
+        W.ncols = B.ncols;
+        cudaFuncSetAttribute(k_bin_scatter_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmem);
+        cudaFuncSetAttribute(k_bin_scatter_w, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_bin_apply_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
       }
       cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
       cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);

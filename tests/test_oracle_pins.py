@@ -463,3 +463,10 @@ def test_union_threshold_accepts_exactly_estimate_ge_theta(theta):
     # θ < g·ln 2 here, so θ_uc < θ_bn: the union option drops exactly the paper output's hosts below θ
     kept = [(int(h["ip"]), int(h["z"])) for h in h0 if h["estimate"] >= theta]
     assert kept == [(int(h["ip"]), int(h["z"])) for h in h1]
+
+
+def test_update_parallel_equals_update(paper):
+    """The threaded oracle driver (private cubes OR-merged) is the single-threaded update."""
+    src, dst = W.random_pairs(400_000, 31)
+    for threads in (1, 3, 8):
+        assert np.array_equal(O.update_parallel(paper, src, dst, threads), O.update(paper, src, dst)[0])

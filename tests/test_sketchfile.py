@@ -78,3 +78,41 @@ def test_gpu_file_equals_oracle_file_and_global_merge(paper):
     with pytest.raises(cb.CbaaError) as e:
         other.deserialize(files[0], merge=True)
     assert e.value.code == cb.E_MISMATCH and "bv_seed" in str(e.value)
+
+
+ODD = dict(r=6, num_ra=2, num_va=2, g=64, cbn=[14, 13, 5, 7], clbs=[0, 13], mangle_a=0x12345679,
+           mangle_b=0xDEADBEEF, bv_seed=0x01020304, va_seeds=[0xA5A5A5A5, 0x0BADF00D], theta_formula=0,
+           tuple_cap=1 << 24, direction=0)
+
+
+def _golden_headers(golden):
+    g = golden("sketch_headers.txt")
+    return {k: bytes(v[0]) for k, v in g.items()}
+
+
+@pytest.mark.parametrize("name", ["paper", "odd"])
+def test_header_golden_bytes(paper, golden, name):
+    """The serializer's header equals the hand-assembled bytes of S:479 (tests/golden/sketch_headers.txt),
+    and the library's parser reads those bytes back to the same geometry and seeds."""
+    p = paper if name == "paper" else dict(paper, **ODD)
+    want = _golden_headers(golden)[name]
+    data = O.serialize(p, np.zeros(O.cube_bytes(p), np.uint8))
+    assert data[:len(want)] == want
+    assert len(data) == len(want) + O.cube_bytes(p)
+    c = cb.sketch_config(want + bytes(O.cube_bytes(p))).to_dict()
+    for k in ("r", "num_ra", "num_va", "g", "cbn", "clbs", "mangle_a", "mangle_b", "bv_seed", "va_seeds"):
+        assert c[k] == p[k], k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["paper", "odd"])
+def test_device_file_header_golden(paper, golden, name):
+    """cbaa_serialize's header from a device cube equals the hand-assembled bytes."""
+    torch = pytest.importorskip("torch")
+    p = paper if name == "paper" else dict(paper, **ODD)
+    h = cb.Cbaa(cb.config_from_dict(p), 0)
+    h.reset()
+    torch.cuda.synchronize()
+    want = _golden_headers(golden)[name]
+    data = h.serialize()
+    assert bytes(data[:len(want)]) == want and not data[len(want):].any()
