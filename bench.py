@@ -605,22 +605,29 @@ def main():
                  "ratio": ((nb.get("update") or {}).get("dram_bytes") or 0) / algo_in if nb.get("update") else None,
                  "source": os.path.relpath(NCU_BINNED, ROOT)},
     }
-    if args.update_mode == "binned":
-        scat = "k_bin_wc" if os.environ.get("CBAA_BIN_SCATTER") == "wc" else "k_bin_scatter"
-        names = ["k_bin_sample|k_bin_count", "k_bin_starts", scat, "k_bin_apply"]
+    plan_s = lat_handle.update_plan(int(per_call_pairs))
+    if plan_s.startswith("binned"):
+        # the kernels the library launched per phase (cbaa_update_plan), e.g. "binned-wide k_bin_sample
+        # k_bin_starts k_bin_scatter_w k_bin_apply_w+k_bin_log_w entry_bytes=8"
+        words = plan_s.split()
+        names, ebytes = words[1:5], int(words[5].split("=")[1])
+        scat = names[2]
         kernels = {}
         for name, t in zip(names, per_call):
             kernels[name] = {"ms": t, "share": t / max(1e-9, sum(per_call))}
         tsc = per_call[2]
-        design = {"k_bin_scatter": 12, "k_bin_wc": 12}[scat]
+        design = 8 + ebytes
         roofline = {"kernel": scat, "bound": "hbm",
                     "achieved": 8 * per_call_pairs / (tsc / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": 8 * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,
                     "traffic": (nb.get(scat) or {}).get("dram_bytes_per_launch"),
+                    "traffic_source": os.path.relpath(NCU_BINNED, ROOT) + " (ncu --set full, dram__bytes_read+write "
+                                      "per launch)",
                     "algorithmic": "SURVEY 8(d): 8 B/pair of input read per launch (pairs per launch x 8 B)",
                     "design_bytes_per_pair": design,
                     "design_frac": design * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,
-                    "design_note": "the binned design also writes a 4 B entry per pair (read back by k_bin_apply)",
+                    "design_note": f"the binned design also writes a {ebytes} B entry per pair (read back by the apply)",
+                    "update_plan": plan_s,
                     "per_launch_ms": tsc,
                     "timing": "CUDA event pair around every update kernel on its launch stream over the timed "
                               "region (cbaa_set_phase_timing), averaged per launch",
@@ -629,7 +636,7 @@ def main():
     else:
         peak_acc = max(peaks_acc.values()) if peaks_acc else None
         achieved = algo_bits / (upd / 1e3)
-        roofline = {"kernel": "k_update", "bound": "lsu_random_word", "achieved": achieved / 1e9,
+        roofline = {"kernel": "k_update", "bound": "lsu_random_word", "achieved": achieved / 1e9, "update_plan": plan_s,
                     "peak": (peak_acc or float("nan")) / 1e9, "unit": "G word-updates/s",
                     "frac": achieved / peak_acc if peak_acc else None, "traffic": None,
                     "peak_source": "tools/redbench --quick in this run (best of random LDG / RED.OR)",

@@ -326,6 +326,12 @@ uint32_t cbaa_update_passes(const cbaa_handle* h);
 int cbaa_set_phase_timing(cbaa_handle* h, int enable);
 int cbaa_update_phase_ms(cbaa_handle* h, double* ms, int cap, uint64_t* calls);
 
+/* The kernels a cbaa_update call of n pairs would launch, per phase, as one NUL-terminated line written
+ * into buf (buflen bytes, truncated): "binned-wide k_bin_sample k_bin_starts k_bin_scatter_w
+ * k_bin_apply_w+k_bin_log_w entry_bytes=8", "binned ... entry_bytes=4", or "direct k_update passes=P".
+ * Host only, no GPU work; CBAA_E_ARG if h or buf is null (bench evidence: which kernel is dominant). */
+int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t buflen);
+
 const char* cbaa_strerror(int code);
 const char* cbaa_last_error(const cbaa_handle* h);
 

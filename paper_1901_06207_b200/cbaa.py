@@ -104,6 +104,7 @@ _SIGS = {
     "cbaa_update_passes": (C.c_uint32, [_h]),
     "cbaa_set_phase_timing": (C.c_int, [_h, C.c_int]),
     "cbaa_update_phase_ms": (C.c_int, [_h, _P(C.c_double), C.c_int, _P(C.c_uint64)]),
+    "cbaa_update_plan": (C.c_int, [_h, C.c_uint64, C.c_char_p, C.c_uint64]),
     "cbaa_strerror": (C.c_char_p, [C.c_int]),
     "cbaa_last_error": (C.c_char_p, [_h]),
 }
@@ -424,6 +425,12 @@ class Cbaa:
     def set_phase_timing(self, enable: bool = True):
         """Event pairs around every update kernel (cbaa_set_phase_timing)."""
         self._check(lib().cbaa_set_phase_timing(self._h, int(enable)), "cbaa_set_phase_timing")
+
+    def update_plan(self, n: int) -> str:
+        """The kernels an update of n pairs launches, per phase (cbaa_update_plan)."""
+        buf = C.create_string_buffer(256)
+        self._check(lib().cbaa_update_plan(self._h, n, buf, 256), "cbaa_update_plan")
+        return buf.value.decode()
 
     def update_phase_ms(self):
         """(ms per phase summed since the last query, update calls): binned [count, starts, scatter, apply],

@@ -1381,6 +1381,24 @@ uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0
 
 uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }
 
+int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t buflen) {
+  if (!h || !buf || !buflen) return CBAA_E_ARG;
+  std::string p;
+  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min) {
+    const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
+    const bool wide = h->bin_wide && !prefix && !h->bin_wc;
+    const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
+    const bool sampled = samp && std::min(n, h->bin_chunk) >= h->bin_sample_min;
+    p = std::string(wide ? "binned-wide " : "binned ") + (sampled ? "k_bin_sample" : "k_bin_count") + " k_bin_starts " +
+        (wide ? "k_bin_scatter_w" : h->bin_wc ? "k_bin_wc" : "k_bin_scatter") + " " +
+        (wide ? "k_bin_apply_w+k_bin_log_w" : "k_bin_apply+k_bin_log") + (wide ? " entry_bytes=8" : " entry_bytes=4");
+  } else {
+    p = "direct k_update passes=" + std::to_string(h->passes);
+  }
+  std::snprintf(buf, buflen, "%s", p.c_str());
+  return CBAA_OK;
+}
+
 int cbaa_set_phase_timing(cbaa_handle* h, int enable) {
   if (!h) return CBAA_E_ARG;
   h->timing = enable ? 1 : 0;
