@@ -159,7 +159,9 @@ int cbaa_create(const cbaa_config* cfg, int device, cbaa_handle** out);
 /* Same, but the cube lives in caller-owned DEVICE memory `cube` (≥ cube_bytes,
  * 256-byte aligned), e.g. a symmetric-memory buffer that peer GPUs map over
  * NVLink so cbaa_merge_slice can pull their slices directly.
- * The memory is zeroed here and never freed by the library. */
+ * The memory is zeroed here and never freed by the library.  With
+ * cube_nbytes ≥ cbaa_signal_offset + CBAA_SIGNAL_BYTES the tail also holds the
+ * signal area of cbaa_peer_barrier (library-owned cubes always have one). */
 int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cube_nbytes, cbaa_handle** out);
 void cbaa_destroy(cbaa_handle* h);
 int cbaa_get_config(const cbaa_handle* h, cbaa_config* out);
@@ -218,6 +220,23 @@ int cbaa_merge(cbaa_handle* h, const void* const* cubes, int k, uint64_t nbytes,
  * Used when each rank owns a CS range. Async on stream. */
 int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
                      cbaa_stream stream);
+
+/* Pull-OR of a CS range fused with the window-end zero counts (a8 + a9, P:249,
+ * P:258-261): like cbaa_merge_slice, and in the same pass over the owned bytes
+ * the zero count of every RA column of [cs_lo, cs_hi) is recorded, so the next
+ * cbaa_detect_range over exactly that range skips its own zero-count pass.  Any
+ * later reset/update/merge discards those counts.  g ≠ 4096 or k > 16: plain
+ * cbaa_merge_slice (the detect counts as usual).  Async on stream. */
+int cbaa_merge_slice_zc(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
+                        cbaa_stream stream);
+
+/* NVLink SHARP (NVLS) merge: mc_cube is the MULTICAST address of a cube buffer
+ * that every rank holds at the same offsets (e.g. torch symmetric memory's
+ * multicast_ptr); the switch ORs the ranks' bytes of CSs [cs_lo, cs_hi)
+ * (multimem.ld_reduce .or.b64) and this handle's cube receives the result.
+ * The caller orders it after every rank's update (cbaa_peer_barrier or the
+ * symmetric-memory barrier).  Requires multicast support.  Async on stream. */
+int cbaa_merge_multicast(cbaa_handle* h, const void* mc_cube, uint32_t cs_lo, uint32_t cs_hi, cbaa_stream stream);
 
 /* ------------------------------------------------------------------- detect */
 
@@ -280,6 +299,31 @@ int cbaa_ipc_export(cbaa_handle* h, void* out);
  * device until cbaa_ipc_close.  The peer cube must have the same geometry. */
 int cbaa_ipc_open(cbaa_handle* h, const void* handle, void** dev_ptr);
 int cbaa_ipc_close(cbaa_handle* h, void* dev_ptr);
+
+/* ------------------------------------------------- device-side router barrier
+ * A cube allocation carries, after the cube (at cbaa_signal_offset bytes from
+ * its start), CBAA_SIGNAL_BYTES of signals: u64 epoch slots (one per rank, at
+ * most 64 ranks) and a u32 status.  Peers reach it through the same mapping as
+ * the cube (CUDA IPC or symmetric memory), so no host round trip is needed. */
+#define CBAA_SIGNAL_BYTES 4096
+uint64_t cbaa_signal_offset(const cbaa_handle* h);
+
+/* Stream-ordered barrier of `world` routers: after every prior operation on
+ * `stream` (the window's update) is complete and visible system-wide, writes
+ * `epoch` (> 0, increasing per barrier) into slot `rank` of every peer's signal
+ * area and waits ON THE DEVICE until all peers have written it into this
+ * handle's.  peer_cubes[k] = rank k's cube base as mapped here (this rank's
+ * entry is ignored).  One one-CTA kernel; after CBAA_BARRIER_TIMEOUT_MS
+ * (default 10000) it stops waiting and sets the status word (cbaa_peer_status)
+ * instead of hanging the GPU.  Async on stream. */
+int cbaa_peer_barrier(cbaa_handle* h, void* const* peer_cubes, int world, int rank, uint64_t epoch,
+                      cbaa_stream stream);
+/* Synchronous read of the status word: 0 = every barrier completed, 1 = one timed out. */
+int cbaa_peer_status(cbaa_handle* h, uint32_t* status);
+
+/* The output order of S:418 (estimate descending, then ip ascending) on a HOST
+ * array, e.g. for host lists gathered from several ranks' detect_range calls. */
+void cbaa_sort_hosts(cbaa_host* hosts, uint64_t n);
 
 /* ---------------------------------------------------------------- inspection */
 

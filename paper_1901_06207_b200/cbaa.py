@@ -100,6 +100,12 @@ _SIGS = {
     "cbaa_ipc_export": (C.c_int, [_h, C.c_void_p]),
     "cbaa_ipc_open": (C.c_int, [_h, C.c_void_p, _P(C.c_void_p)]),
     "cbaa_ipc_close": (C.c_int, [_h, C.c_void_p]),
+    "cbaa_signal_offset": (C.c_uint64, [_h]),
+    "cbaa_peer_barrier": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_int, C.c_uint64, C.c_void_p]),
+    "cbaa_peer_status": (C.c_int, [_h, _P(C.c_uint32)]),
+    "cbaa_merge_slice_zc": (C.c_int, [_h, _P(C.c_void_p), C.c_int, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "cbaa_merge_multicast": (C.c_int, [_h, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "cbaa_sort_hosts": (None, [C.c_void_p, C.c_uint64]),
     "cbaa_kernel_launches": (C.c_uint64, [_h]),
     "cbaa_update_passes": (C.c_uint32, [_h]),
     "cbaa_set_phase_timing": (C.c_int, [_h, C.c_int]),
@@ -303,6 +309,34 @@ class Cbaa:
         self._check(lib().cbaa_merge_slice(self._h, arr, len(ptrs), cs_lo, cs_hi, _stream(stream)),
                     "cbaa_merge_slice")
 
+    def merge_slice_zc(self, slices, cs_lo, cs_hi, stream=None):
+        """merge_slice fused with the window-end zero counts of [cs_lo, cs_hi) (cbaa_merge_slice_zc)."""
+        ptrs = [s if isinstance(s, int) else s.data_ptr() for s in slices]
+        arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+        self._check(lib().cbaa_merge_slice_zc(self._h, arr, len(ptrs), cs_lo, cs_hi, _stream(stream)),
+                    "cbaa_merge_slice_zc")
+
+    def merge_multicast(self, mc_cube: int, cs_lo, cs_hi, stream=None):
+        """NVLS OR of every rank's bytes of CSs [cs_lo, cs_hi) through a multicast address (cbaa_merge_multicast)."""
+        self._check(lib().cbaa_merge_multicast(self._h, C.c_void_p(mc_cube), cs_lo, cs_hi, _stream(stream)),
+                    "cbaa_merge_multicast")
+
+    # ------------------------------------------------------------ device-side router barrier
+    @property
+    def signal_offset(self) -> int:
+        return lib().cbaa_signal_offset(self._h)
+
+    def peer_barrier(self, peer_cubes, world: int, rank: int, epoch: int, stream=None):
+        """Stream-ordered device barrier over the peers' signal areas (cbaa_peer_barrier); peer_cubes[k] =
+        rank k's cube base as mapped here (ignored for k == rank)."""
+        arr = (C.c_void_p * world)(*[p or 0 for p in peer_cubes])
+        self._check(lib().cbaa_peer_barrier(self._h, arr, world, rank, epoch, _stream(stream)), "cbaa_peer_barrier")
+
+    def peer_status(self) -> int:
+        v = C.c_uint32()
+        self._check(lib().cbaa_peer_status(self._h, C.byref(v)), "cbaa_peer_status")
+        return v.value
+
     def detect(self, theta: int, cap: int = 1 << 20, cs_lo: int = 0, cs_hi: int | None = None, stream=None,
                raise_on_overflow: bool = False, with_stats: bool = True):
         """Window end: returns (hosts structured array, per-CS stats list or None, status code)."""
@@ -439,6 +473,14 @@ class Cbaa:
         calls = C.c_uint64()
         self._check(lib().cbaa_update_phase_ms(self._h, ms, 4, C.byref(calls)), "cbaa_update_phase_ms")
         return list(ms), calls.value
+
+
+def sort_hosts(hosts: np.ndarray) -> np.ndarray:
+    """The S:418 output order (estimate descending, ip ascending) of a host array, in the library
+    (cbaa_sort_hosts); returns a sorted copy."""
+    out = np.ascontiguousarray(hosts, dtype=HOST_DTYPE).copy()
+    lib().cbaa_sort_hosts(out.ctypes.data_as(C.c_void_p), out.size)
+    return out
 
 
 def _wrap_device(ptr: int, nbytes: int, device: int, owner):

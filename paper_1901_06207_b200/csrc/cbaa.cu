@@ -33,6 +33,16 @@ struct DetectKey {   // what a captured detect graph depends on (θ is not part 
   }
 };
 
+struct DetectGraph {
+  cudaGraph_t graph = nullptr;          // kept alive: hot_node belongs to it
+  cudaGraphExec_t exec = nullptr;
+  DetectKey key{};
+  cudaGraphNode_t hot_node = nullptr;   // the k_hot node: θ is set per detect by a kernel-node parameter update
+  cudaKernelNodeParams hot_params{};
+  uint32_t theta = 0;                   // θ currently in the instantiated graph
+  int kernels = 0;
+};
+
 struct cbaa_handle {
   cbaa_config cfg;
   Geo G;
@@ -66,15 +76,14 @@ struct cbaa_handle {
   uint64_t stage_pairs = 0;
   uint64_t launches = 0;
   int upd_blocks = 0;
-  // detect graph (captured on cap_stream, launched on the caller's stream)
+  // detect graphs (captured on cap_stream, launched on the caller's stream): [0] full, [1] without the
+  // zero-count pass (its counts came from cbaa_merge_slice_zc)
   cudaStream_t cap_stream = nullptr;
-  cudaGraph_t graph = nullptr;          // kept alive: hot_node belongs to it
-  cudaGraphExec_t graph_exec = nullptr;
-  DetectKey graph_key{};
-  cudaGraphNode_t hot_node = nullptr;   // the k_hot node: θ is set per detect by a kernel-node parameter update
-  cudaKernelNodeParams hot_params{};
-  uint32_t graph_theta = 0;             // θ currently in the instantiated graph
-  int graph_kernels = 0;
+  DetectGraph dgs[2];
+  int zc_fresh = 0;                     // zc holds the zero counts of CSs [zc_lo, zc_hi) of the current cube
+  uint32_t zc_lo = 0, zc_hi = 0;
+  // device barrier (cbaa_peer_barrier): signal area after the cube in the same allocation
+  unsigned long long* sig = nullptr;
   int use_join = 0;          // |RA| = 3 and not forced Cartesian
   // binned update (CBAA_UPDATE_BINNED, binned.cuh)
   BinGeo B{};
@@ -630,6 +639,8 @@ uint64_t cbaa_cube_bytes(const cbaa_config* cfg) {
   return (csb << cfg->r) / 8;
 }
 
+static uint64_t sig_offset(uint64_t cube_bytes) { return (cube_bytes + 255) & ~255ull; }
+
 int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cube_nbytes, cbaa_handle** out) {
   if (!out) return CBAA_E_ARG;
   *out = nullptr;
@@ -662,13 +673,21 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     }
     h->cube = (uint32_t*)cube;
     h->cube_external = true;
+    if (cube_nbytes >= sig_offset(h->cube_bytes) + kSigBytes)   // room for the barrier's signal area
+      h->sig = (unsigned long long*)((char*)cube + sig_offset(h->cube_bytes));
   } else {
-    e = cudaMalloc(&h->cube, h->cube_bytes);
+    // the cube and, after it, the signal area of cbaa_peer_barrier: one allocation, one IPC handle
+    e = cudaMalloc(&h->cube, sig_offset(h->cube_bytes) + kSigBytes);
     if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMalloc(cube)");
+    else h->sig = (unsigned long long*)((char*)h->cube + sig_offset(h->cube_bytes));
   }
   if (!rc) {
     e = cudaMemset(h->cube, 0, h->cube_bytes);
     if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemset(cube)");
+  }
+  if (!rc && h->sig) {
+    e = cudaMemset(h->sig, 0, kSigBytes);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemset(signals)");
   }
   if (!rc) rc = alloc_scratch(h);
   if (!rc && cfg->direction == CBAA_DIR_INNER_PREFIX) rc = upload_prefix_bits(h);
@@ -797,8 +816,10 @@ void cbaa_destroy(cbaa_handle* h) {
     if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
   }
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-  if (h->graph) cudaGraphDestroy(h->graph);
+  for (DetectGraph& d : h->dgs) {
+    if (d.exec) cudaGraphExecDestroy(d.exec);
+    if (d.graph) cudaGraphDestroy(d.graph);
+  }
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
 }
@@ -811,6 +832,7 @@ int cbaa_get_config(const cbaa_handle* h, cbaa_config* out) {
 
 int cbaa_reset(cbaa_handle* h, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t n16 = h->cube_bytes / 16;
@@ -823,6 +845,7 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream) {
 
 int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (n == 0) return CBAA_OK;
   if (!src || !dst) return fail(h, CBAA_E_ARG, "cbaa_update: null src/dst");
   if (((uintptr_t)src | (uintptr_t)dst) & 3) return fail(h, CBAA_E_ARG, "cbaa_update: src/dst must be 4-byte aligned");
@@ -832,6 +855,7 @@ int cbaa_update(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64
 
 int cbaa_update_pairs(cbaa_handle* h, const uint32_t* pairs, uint64_t n, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (n == 0) return CBAA_OK;
   if (!pairs) return fail(h, CBAA_E_ARG, "cbaa_update_pairs: null pairs");
   if ((uintptr_t)pairs & 7) return fail(h, CBAA_E_ARG, "cbaa_update_pairs: pairs must be 8-byte aligned");
@@ -847,6 +871,7 @@ int cbaa_update_pairs(cbaa_handle* h, const uint32_t* pairs, uint64_t n, cbaa_st
 
 int cbaa_update_host(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (n == 0) return CBAA_OK;
   if (!src || !dst) return fail(h, CBAA_E_ARG, "cbaa_update_host: null src/dst");
   DeviceGuard dg(h->device);
@@ -892,6 +917,7 @@ int cbaa_skipped(cbaa_handle* h, uint64_t* out, cbaa_stream stream) {
 
 int cbaa_merge(cbaa_handle* h, const void* const* cubes, int k, uint64_t nbytes, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (k < 0 || k > CBAA_MAX_MERGE || (k && !cubes)) return fail(h, CBAA_E_ARG, "cbaa_merge: bad k/cubes");
   if (nbytes != h->cube_bytes)
     return fail(h, CBAA_E_MISMATCH, "cbaa_merge: cube size differs from this handle's geometry (S:103)");
@@ -916,6 +942,7 @@ int cbaa_merge(cbaa_handle* h, const void* const* cubes, int k, uint64_t nbytes,
 int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
                      cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (cs_lo >= cs_hi || cs_hi > h->G.n_cs) return fail(h, CBAA_E_ARG, "cbaa_merge_slice: bad CS range");
   if (k < 0 || k > CBAA_MAX_MERGE || (k && !slices)) return fail(h, CBAA_E_ARG, "cbaa_merge_slice: bad k/slices");
   DeviceGuard dg(h->device);
@@ -939,7 +966,7 @@ int cbaa_merge_slice(cbaa_handle* h, const void* const* slices, int k, uint32_t 
 }
 
 static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uint32_t theta, int finish,
-                           cudaStream_t s, int join = 0) {
+                           cudaStream_t s, int join = 0, int zc_given = 0) {
   const Geo& G = h->G;
   uint64_t groups = 0;
   for (uint32_t i = 0; i < G.num_ra; ++i) groups += (G.ncols[i] + 15) / 16;
@@ -949,13 +976,15 @@ static int launch_zero_hot(cbaa_handle* h, uint32_t cs_lo, uint32_t n_range, uin
   // g = 4096 with RA blocks of whole 16-column tiles (every c(i) ≥ 16): TMA-streamed zero counts
   bool tma = G.wpc == 128 && !h->no_tma && !h->cfg.detect_overlap;
   for (uint32_t i = 0; i < G.num_ra; ++i) tma = tma && G.ncols[i] % kZcTileCols == 0;
-  if (tma)
+  if (zc_given)
+    ;   // counts (and the per-detect counter reset) came from k_or_merge_zc
+  else if (tma)
     k_zero_counts_tma<<<h->sms * 4, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   else if (G.wpc == 128)   // g = 4096: one 16-byte load per lane covers a column
     k_zero_counts<true><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
   else
     k_zero_counts<false><<<grid, kDetThreads, 0, s>>>(G, h->cube, h->D, cs_lo, n_range, finish);
-  int rc = launch_check(h, "k_zero_counts");
+  int rc = zc_given ? CBAA_OK : launch_check(h, "k_zero_counts");
   if (rc || !finish) return rc;
   const uint64_t hot_grid = (uint64_t)n_range * G.num_ra;
   if (hot_grid > 0x7fffffffull) return fail(h, CBAA_E_ARG, "detect grid too large");
@@ -984,19 +1013,24 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   DetectScratch& D = h->D;
   // The whole device side of a detect — zeroing, zero counts, k_hot, the Alg. 3 kernels and the copy
   // of the CS records and [n_hits | first kFirst hits] to pinned memory — is one CUDA graph, captured
-  // once per (range, θ, buffers) and relaunched every window: one launch and one host sync per detect.
+  // once per (range, buffers) and relaunched every window (θ rewritten in place): one launch and one
+  // host sync per detect.
   const uint64_t kFirst = std::min<uint64_t>(1024, D.hit_cap);
+  // zero counts already computed by cbaa_merge_slice_zc for exactly this range: the graph without them
+  const int zg = (h->zc_fresh && h->zc_lo == cs_lo && h->zc_hi == cs_hi) ? 1 : 0;
+  h->zc_fresh = 0;   // consumed: that kernel also zeroed the per-detect counters, once
+  DetectGraph& dgr = h->dgs[zg];
   const DetectKey key{cs_lo, cs_hi, h->record, (const void*)D.cand, (const void*)h->h_res, h->use_join};
-  if (!h->graph_exec || !(h->graph_key == key)) {
-    if (h->graph_exec) {
-      cudaGraphExecDestroy(h->graph_exec);
-      h->graph_exec = nullptr;
+  if (!dgr.exec || !(dgr.key == key)) {
+    if (dgr.exec) {
+      cudaGraphExecDestroy(dgr.exec);
+      dgr.exec = nullptr;
     }
-    if (h->graph) {
-      cudaGraphDestroy(h->graph);
-      h->graph = nullptr;
+    if (dgr.graph) {
+      cudaGraphDestroy(dgr.graph);
+      dgr.graph = nullptr;
     }
-    h->hot_node = nullptr;
+    dgr.hot_node = nullptr;
     if (!h->cap_stream) CK(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     cudaStream_t c = h->cap_stream;
     CK(h, cudaStreamBeginCapture(c, cudaStreamCaptureModeThreadLocal));
@@ -1004,7 +1038,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
     // |RA| = 3: range join over the sorted hot lists, then one warp per chain; otherwise (or after a
     // join-buffer overflow) the Cartesian enumeration with the union check inline
     const int join = h->use_join;
-    int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c, join);
+    int rc = launch_zero_hot(h, cs_lo, n_range, theta, 1, c, join, zg);
     const int grid = h->sms * 8;
     if (!rc) {
       if (join) {
@@ -1035,12 +1069,12 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
       return rc;
     }
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaStreamEndCapture(detect)");
-    e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+    e = cudaGraphInstantiate(&dgr.exec, graph, 0);
     if (e != cudaSuccess) {
       cudaGraphDestroy(graph);
       return cuda_fail(h, e, "cudaGraphInstantiate(detect)");
     }
-    h->graph = graph;
+    dgr.graph = graph;
     // find the k_hot node: a later θ only rewrites that node's parameters in the executable graph
     size_t nn = 0;
     CK(h, cudaGraphGetNodes(graph, nullptr, &nn));
@@ -1053,29 +1087,29 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
       cudaKernelNodeParams kp{};
       CK(h, cudaGraphKernelNodeGetParams(nd, &kp));
       if (kp.func == (void*)k_hot) {
-        h->hot_node = nd;
-        h->hot_params = kp;
+        dgr.hot_node = nd;
+        dgr.hot_params = kp;
       }
     }
-    if (!h->hot_node) return fail(h, CBAA_E_CUDA, "detect graph: k_hot node not found");
-    h->graph_theta = theta;
-    h->graph_key = key;
-    h->graph_kernels = (join ? 4 : 3) + (h->cfg.detect_overlap ? 0 : 1);
-    h->launches -= h->graph_kernels;   // counted at capture; counted again per graph launch below
+    if (!dgr.hot_node) return fail(h, CBAA_E_CUDA, "detect graph: k_hot node not found");
+    dgr.theta = theta;
+    dgr.key = key;
+    dgr.kernels = (join ? 4 : 3) - zg + (h->cfg.detect_overlap ? 0 : 1);
+    h->launches -= dgr.kernels;   // counted at capture; counted again per graph launch below
   }
-  if (h->graph_theta != theta) {   // same graph, new θ: k_hot(G, D, cs_lo, n_range, theta, join)
+  if (dgr.theta != theta) {   // same graph, new θ: k_hot(G, D, cs_lo, n_range, theta, join)
     void* args[6];
-    for (int i = 0; i < 6; ++i) args[i] = h->hot_params.kernelParams[i];
+    for (int i = 0; i < 6; ++i) args[i] = dgr.hot_params.kernelParams[i];
     uint32_t th = theta;
     args[4] = &th;
-    cudaKernelNodeParams kp = h->hot_params;
+    cudaKernelNodeParams kp = dgr.hot_params;
     kp.kernelParams = args;
     kp.extra = nullptr;
-    CK(h, cudaGraphExecKernelNodeSetParams(h->graph_exec, h->hot_node, &kp));
-    h->graph_theta = theta;
+    CK(h, cudaGraphExecKernelNodeSetParams(dgr.exec, dgr.hot_node, &kp));
+    dgr.theta = theta;
   }
-  CK(h, cudaGraphLaunch(h->graph_exec, s));
-  h->launches += h->graph_kernels;
+  CK(h, cudaGraphLaunch(dgr.exec, s));
+  h->launches += dgr.kernels;
   CK(h, cudaStreamSynchronize(s));
   if (h->use_join && ((const unsigned long long*)h->h_res)[1] > D.join_cap) {
     // more CP chains than the join buffer holds: redo this window with the Cartesian enumeration
@@ -1104,11 +1138,7 @@ int cbaa_detect_range(cbaa_handle* h, uint32_t theta, uint32_t cs_lo, uint32_t c
   }
   // output order of S:418: estimate descending, then ip ascending (already done on the device for a
   // standalone detect of at most kSortMax hits)
-  if (h->cfg.detect_overlap || got > (uint64_t)kSortMax)
-    std::sort(h->h_hits, h->h_hits + got, [](const cbaa_host& a, const cbaa_host& b) {
-      if (a.estimate != b.estimate) return a.estimate > b.estimate;
-      return a.ip < b.ip;
-    });
+  if (h->cfg.detect_overlap || got > (uint64_t)kSortMax) cbaa_sort_hosts(h->h_hits, got);
   const uint64_t ncopy = std::min<uint64_t>(got, cap);
   if (ncopy) std::memcpy(out, h->h_hits, ncopy * sizeof(cbaa_host));
   *n_out = total;
@@ -1295,6 +1325,7 @@ int cbaa_sketch_config(const void* in, uint64_t n, cbaa_config* out, char* err, 
 
 int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_stream stream) {
   if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;   // the cube changes: zero counts of an earlier pull-OR are stale
   if (mode != CBAA_SKETCH_REPLACE && mode != CBAA_SKETCH_MERGE) return fail(h, CBAA_E_ARG, "bad mode");
   cbaa_config fc;
   const uint8_t* payload = nullptr;
@@ -1350,6 +1381,7 @@ int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_
 
 // ------------------------------------------------------------------ peer cubes (CUDA IPC)
 static_assert(sizeof(cudaIpcMemHandle_t) == CBAA_IPC_HANDLE_BYTES, "IPC handle size");
+static_assert(kSigBytes == CBAA_SIGNAL_BYTES && (kMaxRanks + 1) * 8 <= kSigBytes, "signal area");
 
 int cbaa_ipc_export(cbaa_handle* h, void* out) {
   if (!h || !out) return CBAA_E_ARG;
@@ -1375,6 +1407,82 @@ int cbaa_ipc_close(cbaa_handle* h, void* dev_ptr) {
   DeviceGuard dg(h->device);
   CK(h, cudaIpcCloseMemHandle(dev_ptr));
   return CBAA_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU window end
+uint64_t cbaa_signal_offset(const cbaa_handle* h) { return h ? sig_offset(h->cube_bytes) : 0; }
+
+int cbaa_peer_barrier(cbaa_handle* h, void* const* peer_cubes, int world, int rank, uint64_t epoch,
+                      cbaa_stream stream) {
+  if (!h || !peer_cubes || world < 1 || world > kMaxRanks || rank < 0 || rank >= world || epoch == 0)
+    return fail(h, CBAA_E_ARG, "cbaa_peer_barrier: bad arguments");
+  if (!h->sig) return fail(h, CBAA_E_ARG, "cbaa_peer_barrier: caller memory without room for the signal area");
+  DeviceGuard dg(h->device);
+  PeerSigs P{};
+  for (int k = 0; k < world; ++k) {
+    char* base = k == rank ? (char*)h->cube : (char*)peer_cubes[k];
+    if (!base) return fail(h, CBAA_E_ARG, "cbaa_peer_barrier: null peer cube");
+    P.sig[k] = (unsigned long long*)(base + sig_offset(h->cube_bytes));
+  }
+  const char* to = std::getenv("CBAA_BARRIER_TIMEOUT_MS");
+  const unsigned long long ns = 1000000ull * (to ? std::strtoull(to, nullptr, 10) : 10000ull);
+  k_peer_barrier<<<1, kMaxRanks, 0, (cudaStream_t)stream>>>(P, world, rank, (unsigned long long)epoch, ns,
+                                                             (uint32_t*)(h->sig + kMaxRanks));
+  return launch_check(h, "k_peer_barrier");
+}
+
+int cbaa_peer_status(cbaa_handle* h, uint32_t* status) {
+  if (!h || !status || !h->sig) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  CK(h, cudaMemcpy(status, h->sig + kMaxRanks, 4, cudaMemcpyDeviceToHost));
+  return CBAA_OK;
+}
+
+int cbaa_merge_slice_zc(cbaa_handle* h, const void* const* slices, int k, uint32_t cs_lo, uint32_t cs_hi,
+                        cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  if (h->G.wpc != 128 || k > 16)   // fused kernel: g = 4096, ≤ 16 peers; otherwise merge, detect counts
+    return cbaa_merge_slice(h, slices, k, cs_lo, cs_hi, stream);
+  h->zc_fresh = 0;
+  if (cs_lo >= cs_hi || cs_hi > h->G.n_cs) return fail(h, CBAA_E_ARG, "cbaa_merge_slice_zc: bad CS range");
+  if (k < 0 || (k && !slices)) return fail(h, CBAA_E_ARG, "cbaa_merge_slice_zc: bad k/slices");
+  DeviceGuard dg(h->device);
+  MergeSrcs S{};
+  S.k = k;
+  for (int j = 0; j < k; ++j) {
+    if (!slices[j] || ((uintptr_t)slices[j] & 15))
+      return fail(h, CBAA_E_ARG, "cbaa_merge_slice_zc: null or non-16-byte-aligned slice pointer");
+    S.p[j] = (const uint4*)slices[j];
+  }
+  const uint64_t cols = (uint64_t)(cs_hi - cs_lo) * (h->G.cs_words >> h->G.wpc_log2);
+  const int grid = (int)std::min<uint64_t>((uint64_t)h->sms * 8, (cols + kDetWarps - 1) / kDetWarps);
+  k_or_merge_zc<<<grid, kDetThreads, 0, (cudaStream_t)stream>>>(h->G, h->cube, S, cs_lo, cs_hi - cs_lo, h->D);
+  int rc = launch_check(h, "k_or_merge_zc");
+  if (rc) return rc;
+  h->zc_fresh = 1;
+  h->zc_lo = cs_lo;
+  h->zc_hi = cs_hi;
+  return CBAA_OK;
+}
+
+int cbaa_merge_multicast(cbaa_handle* h, const void* mc_cube, uint32_t cs_lo, uint32_t cs_hi, cbaa_stream stream) {
+  if (!h) return CBAA_E_ARG;
+  h->zc_fresh = 0;
+  if (!mc_cube || ((uintptr_t)mc_cube & 15)) return fail(h, CBAA_E_ARG, "cbaa_merge_multicast: bad multicast address");
+  if (cs_lo >= cs_hi || cs_hi > h->G.n_cs) return fail(h, CBAA_E_ARG, "cbaa_merge_multicast: bad CS range");
+  DeviceGuard dg(h->device);
+  const uint64_t csb = (uint64_t)h->G.cs_words * 4, off = csb * cs_lo, n8 = csb * (cs_hi - cs_lo) / 8;
+  k_or_multicast<<<grid_for(h, n8, 4), kThreads, 0, (cudaStream_t)stream>>>(
+      (uint64_t*)((char*)h->cube + off), (const uint64_t*)((const char*)mc_cube + off), n8);
+  return launch_check(h, "k_or_multicast");
+}
+
+void cbaa_sort_hosts(cbaa_host* hosts, uint64_t n) {
+  if (!hosts || n < 2) return;
+  std::sort(hosts, hosts + n, [](const cbaa_host& a, const cbaa_host& b) {
+    if (a.estimate != b.estimate) return a.estimate > b.estimate;
+    return a.ip < b.ip;
+  });
 }
 
 uint64_t cbaa_kernel_launches(const cbaa_handle* h) { return h ? h->launches : 0; }

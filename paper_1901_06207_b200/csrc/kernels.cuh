@@ -943,3 +943,103 @@ __global__ void k_debug_map(const __grid_constant__ Geo G, const uint32_t* __res
 }
 
 }  // namespace cbaa
+
+namespace cbaa {
+// ---------------------------------------------------------------- window-end exchange across GPUs
+// Signal area of a cube allocation (after the cube, 256-B aligned): u64 epoch[kMaxRanks] written by the
+// peers (slot k by rank k) + u32 status (non-zero: a barrier timed out).
+constexpr int kMaxRanks = 64;
+constexpr uint64_t kSigBytes = 4096;
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct PeerSigs {
+  unsigned long long* sig[kMaxRanks];   // rank k's signal area as mapped here (NVLink P2P / IPC)
+};
+
+// Device-side barrier of the routers' streams: every prior kernel on this stream has finished (stream
+// order) and its cube writes are made visible system-wide, then rank `rank` writes `epoch` into slot
+// `rank` of every peer's signal area and waits until every peer has written it into its own.  One CTA;
+// gives up after timeout_ns (status := 1) instead of spinning forever.
+__global__ void k_peer_barrier(const __grid_constant__ PeerSigs P, int world, int rank, unsigned long long epoch,
+                               unsigned long long timeout_ns, uint32_t* status) {
+  __threadfence_system();
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < world) st_release_sys(P.sig[t] + rank, epoch);
+  if (t < world) {
+    const unsigned long long* mine = P.sig[rank] + t;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(mine) < epoch) {
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(status, 1u);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
+// Pull-OR of the owner's CS range fused with the window-end zero counts (a8 + a9): one warp per column,
+// g = 4096 (a column = 512 B = one 16-B load per lane): own | peer_0 | … | peer_{k−1} is stored back and,
+// for RA columns, g − popcount is written to zc — the detect that follows skips its zero-count pass.
+// Block 0 also zeroes the per-detect counters (as k_zero_counts does).
+__global__ void __launch_bounds__(kDetThreads) k_or_merge_zc(const __grid_constant__ Geo G, uint32_t* __restrict__ cube,
+                                                          const __grid_constant__ MergeSrcs S, uint32_t cs_lo,
+                                                          uint32_t n_range, const __grid_constant__ DetectScratch D) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t cols_per_cs = G.cs_words >> G.wpc_log2;
+  const uint64_t total = (uint64_t)n_range * cols_per_cs;
+  if (blockIdx.x == 0) zero_detect_counters(D, cs_lo, n_range);
+  const uint64_t n_warps = ((uint64_t)gridDim.x * kDetThreads) >> 5;
+  for (uint64_t c = ((uint64_t)blockIdx.x * kDetThreads + threadIdx.x) >> 5; c < total; c += n_warps) {
+    const uint32_t cs = cs_lo + (uint32_t)(c / cols_per_cs), col = (uint32_t)(c % cols_per_cs);
+    const uint64_t w0 = (uint64_t)cs * G.cs_words + ((uint64_t)col << G.wpc_log2);
+    uint4* dst = reinterpret_cast<uint4*>(cube + w0) + lane;
+    uint4 a = *dst;
+    const uint64_t off16 = (w0 - (uint64_t)cs_lo * G.cs_words) / 4 + lane;   // slices start at cs_lo
+#pragma unroll 4
+    for (int j = 0; j < S.k; ++j) {
+      const uint4 b = __ldcs(S.p[j] + off16);
+      a.x |= b.x, a.y |= b.y, a.z |= b.z, a.w |= b.w;
+    }
+    *dst = a;
+    const uint32_t pop = warp_sum(__popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w));
+    if (lane == 0 && col < G.ra_cols) D.zc[(size_t)cs * G.ra_cols + col] = G.g - pop;   // RA blocks come first
+  }
+}
+
+// NVLS: the switch ORs the same 8 bytes of every rank's buffer (multimem.ld_reduce on a multicast
+// address, NVLink SHARP); the owner stores the result into its own cube slice.
+__device__ __forceinline__ unsigned long long mc_or(const uint64_t* p) {
+  unsigned long long v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.or.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void k_or_multicast(uint64_t* __restrict__ dst, const uint64_t* __restrict__ mc, uint64_t n8) {
+  constexpr int kU = 4;   // independent switch reductions in flight per thread
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kU - 1) * stride < n8; i += kU * stride) {
+    unsigned long long v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = mc_or(mc + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n8; i += stride) dst[i] = mc_or(mc + i);
+}
+}  // namespace cbaa

@@ -46,11 +46,12 @@ def exchange_owned(cube, rank: int, world: int, n_cs: int, cs_bytes: int, merge_
 
 
 class PeerExchange:
-    """The exchange without a staging collective: every rank's cube lives in torch symmetric memory,
-    so after a device-side barrier the owner's ``cbaa_merge_slice`` kernel reads the peers' slices of
-    its CS range directly over NVLink (peer loads) and ORs them into its own — one kernel for the
-    transfer and the OR.  A second barrier keeps any rank from resetting its cube for the next window
-    while a peer may still be reading it."""
+    """The exchange without a staging collective: every rank's cube lives in torch symmetric memory.
+    After the symmetric-memory device barrier the owner either lets the NVSwitch OR all ranks' bytes of
+    its CS range (NVLS ``multimem.ld_reduce``, ``cbaa_merge_multicast``) when the buffer has a multicast
+    address, or pulls the peers' slices over NVLink and ORs them with its own in one kernel that also
+    computes the window-end zero counts (``cbaa_merge_slice_zc``).  A second barrier keeps any rank from
+    resetting its cube for the next window while a peer may still be reading it."""
 
     def __init__(self, nbytes: int, device, group=None):
         import torch
@@ -61,13 +62,17 @@ class PeerExchange:
         self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
         self.hdl = symm_mem.rendezvous(self.buf, self.group)
         self.ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+        self.mc = int(getattr(self.hdl, "multicast_ptr", 0) or 0)
 
     def exchange(self, cb, rank: int, world: int, n_cs: int, cs_bytes: int, stream):
         lo, hi = owned_range(rank, world, n_cs)
         self.hdl.barrier(channel=0)               # every router's update is complete and visible
-        peers = [p + lo * cs_bytes for k, p in enumerate(self.ptrs) if k != rank]
-        if peers and hi > lo:
-            cb.merge_slice(peers, lo, hi, stream=stream)
+        if hi > lo and world > 1:
+            if self.mc:
+                cb.merge_multicast(self.mc, lo, hi, stream=stream)
+            else:
+                cb.merge_slice_zc([p + lo * cs_bytes for k, p in enumerate(self.ptrs) if k != rank], lo, hi,
+                                  stream=stream)
         return lo, hi
 
     def window_done(self):
@@ -75,36 +80,47 @@ class PeerExchange:
 
 
 class IpcExchange:
-    """The same pull-OR over CUDA IPC mappings of the peers' library-owned cubes (no torch symmetric
-    memory needed; works between processes on one device too).  Synchronisation is host-side: the
-    window's work on the stream is finished, then a process-group barrier, then the owner's merge
-    kernel reads the peers' slices; ``window_done`` fences the next reset the same way."""
+    """The pull-OR over CUDA IPC mappings of the peers' library-owned cubes (no torch symmetric memory
+    needed; works between processes on one device too).  Synchronisation stays on the device: each cube
+    allocation carries a signal area, and ``cbaa_peer_barrier`` (one CTA, stream-ordered after the
+    window's update) raises this rank's epoch in every peer's area and waits for theirs — no host
+    round trip in the window.  Then the owner's ``cbaa_merge_slice_zc`` reads the peers' slices of its CS
+    range over NVLink, ORs them in and records the zero counts; ``window_done`` is a second device
+    barrier that fences the next reset.  ``device_barrier=False`` falls back to stream sync + a
+    process-group barrier (the round-1 scheme)."""
 
-    def __init__(self, cb, rank: int, world: int, group=None):
+    def __init__(self, cb, rank: int, world: int, group=None, device_barrier: bool = True):
         import torch.distributed as dist
 
         self.cb, self.rank, self.world, self.group = cb, rank, world, group
+        self.device_barrier = device_barrier
         handles = [None] * world
         dist.all_gather_object(handles, cb.ipc_export(), group=group)
         self.ptrs = [None if k == rank else cb.ipc_open(hd) for k, hd in enumerate(handles)]
+        self.epoch = 0
 
-    def exchange(self, cb, rank: int, world: int, n_cs: int, cs_bytes: int, stream):
+    def _barrier(self, stream):
         import torch.distributed as dist
 
+        if self.device_barrier:
+            self.epoch += 1
+            self.cb.peer_barrier(self.ptrs, self.world, self.rank, self.epoch, stream=stream)
+        else:
+            stream.synchronize()
+            dist.barrier(group=self.group)
+
+    def exchange(self, cb, rank: int, world: int, n_cs: int, cs_bytes: int, stream):
         lo, hi = owned_range(rank, world, n_cs)
-        stream.synchronize()
-        dist.barrier(group=self.group)            # every router's update is complete
+        self._barrier(stream)                     # every router's update is complete and visible
         peers = [p + lo * cs_bytes for p in self.ptrs if p is not None]
         if peers and hi > lo:
-            cb.merge_slice(peers, lo, hi, stream=stream)
+            cb.merge_slice_zc(peers, lo, hi, stream=stream)
         return lo, hi
 
     def window_done(self, stream=None):
-        import torch.distributed as dist
+        import torch
 
-        if stream is not None:
-            stream.synchronize()
-        dist.barrier(group=self.group)            # peers are done reading before the next reset
+        self._barrier(stream if stream is not None else torch.cuda.current_stream())   # peers done reading
 
     def close(self):
         for p in self.ptrs:
@@ -124,4 +140,5 @@ def gather_hosts(hosts: np.ndarray, rank: int, world: int, group=None):
     if rank != 0:
         return None
     allh = np.concatenate(objs) if objs else hosts[:0]
-    return allh[np.lexsort((allh["ip"], -allh["estimate"]))]
+    from .cbaa import sort_hosts
+    return sort_hosts(allh)   # S:418 order, in the library (cbaa_sort_hosts)

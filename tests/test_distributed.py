@@ -60,7 +60,8 @@ def _worker(rank, world, port, policy, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world, policy", [(2, "hash-by-pair"), (2, "round-robin"), (4, "hash-by-inner")])
+@pytest.mark.parametrize("world, policy", [(2, "hash-by-pair"), (2, "round-robin"), (4, "hash-by-inner"),
+                                           (8, "hash-by-pair")])
 def test_gloo_exchange_matches_global_oracle(tmp_path, world, policy):
     mp.spawn(_worker, args=(world, _free_port(), policy, str(tmp_path)), nprocs=world, join=True)
     p = small_params()

@@ -99,9 +99,9 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
     if exchange == "p2p":
         peer = D.PeerExchange(cube_bytes(cfg), torch.device("cuda", 0))
         cb = Cbaa(cfg, 0, cube=peer.buf)
-    elif exchange == "ipc":
+    elif exchange in ("ipc", "ipc_host"):
         cb = Cbaa(cfg, 0)
-        peer = D.IpcExchange(cb, rank, world)
+        peer = D.IpcExchange(cb, rank, world, device_barrier=exchange == "ipc")
     else:
         peer, cb = None, Cbaa(cfg, 0)
     stream = torch.cuda.Stream()
@@ -119,10 +119,11 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
         hosts, stats, rc = cb.detect(1024, cs_lo=lo, cs_hi=hi, stream=stream)
         if exchange == "p2p":
             peer.window_done()
-        elif exchange == "ipc":
+        elif exchange in ("ipc", "ipc_host"):
             peer.window_done(stream)
     torch.cuda.synchronize()
-    if exchange == "ipc":
+    if exchange in ("ipc", "ipc_host"):
+        assert cb.peer_status() == 0
         peer.close()
     np.save(os.path.join(out_dir, f"src{rank}.npy"), w.src)
     np.save(os.path.join(out_dir, f"dst{rank}.npy"), w.dst)
@@ -134,7 +135,7 @@ def _two_rank_worker(rank, world, port, out_dir, exchange):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["ipc", "p2p", "host"])
+@pytest.mark.parametrize("exchange", ["ipc", "ipc_host", "p2p", "host"])
 def test_two_ranks_one_gpu(tmp_path, exchange):
     """Two router processes sharing one B200: the pull-OR over CUDA IPC mappings of the peer's cube (ipc)
     end to end — handle exchange, barriers, merge_slice reading the peer's memory — the staged path
@@ -164,3 +165,67 @@ def test_two_ranks_one_gpu(tmp_path, exchange):
     hosts = np.load(tmp_path / "hosts.npy", allow_pickle=True)
     assert hosts["ip"].tolist() == ref["ip"].tolist()
     assert np.allclose(hosts["estimate"], ref["estimate"], rtol=1e-12)
+
+
+# ------------------------------------------------------------------ device-side barrier, fused pull-OR
+def test_peer_barrier_orders_peer_reads(paper):
+    """Two routers in one process (two handles, two streams): router 1's merge reads router 0's cube
+    right after a cbaa_peer_barrier on each stream; the barrier alone orders router 0's update before
+    that read (no host synchronisation between them), for three consecutive epochs."""
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
+    a, b = Cbaa(config_from_dict(paper), 0), Cbaa(config_from_dict(paper), 0)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    csb = a.nbytes // 16
+    for epoch, seed in ((1, 3), (2, 4), (3, 5)):
+        src, dst = W.random_pairs(3_000_000, seed)
+        s_t, d_t = (torch.from_numpy(x.view(np.int32)).cuda() for x in (src, dst))
+        torch.cuda.synchronize()
+        a.reset(sa)
+        b.reset(sb)
+        a.update(s_t, d_t, sa)                                    # router 0's window (B has none)
+        a.peer_barrier([None, b.cube_ptr()], 2, 0, epoch, sa)
+        b.peer_barrier([a.cube_ptr(), None], 2, 1, epoch, sb)
+        b.merge_slice([a.cube_ptr() + 8 * csb], 8, 16, sb)        # pulls router 0's CSs 8..15
+        torch.cuda.synchronize()
+        ref, _ = O.update(paper, src, dst)
+        got = b.cube().cpu().numpy()
+        assert np.array_equal(got[8 * csb:], ref[8 * csb:]) and not got[: 8 * csb].any()
+    assert a.peer_status() == 0 and b.peer_status() == 0
+
+
+def test_peer_barrier_times_out_instead_of_hanging(paper, monkeypatch):
+    """A peer that never arrives: the barrier kernel gives up after CBAA_BARRIER_TIMEOUT_MS and flags it."""
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
+    monkeypatch.setenv("CBAA_BARRIER_TIMEOUT_MS", "50")
+    a, b = Cbaa(config_from_dict(paper), 0), Cbaa(config_from_dict(paper), 0)
+    a.peer_barrier([None, b.cube_ptr()], 2, 0, 1)
+    torch.cuda.synchronize()
+    assert a.peer_status() == 1 and b.peer_status() == 0
+
+
+@pytest.mark.parametrize("lo, hi", [(0, 16), (4, 12), (15, 16)])
+def test_merge_slice_zc_then_detect(paper, lo, hi):
+    """The pull-OR fused with the zero counts: the cube slice, the zero counts and the owned-range detect
+    equal the oracle of the OR of both routers' streams; a second detect (counts recomputed) agrees."""
+    from paper_1901_06207_b200.cbaa import Cbaa, config_from_dict
+    from tests.test_gpu_parity import assert_hosts_equal, assert_stats_equal
+    w = W.generate(W.WindowSpec(n=1_200_000, n_hosts=30000, n_flows=200000, scanners=(2500,) * 40), 31)
+    part = W.partition(w.src.size, 2, "hash-by-pair", w.src, w.dst)
+    hs = [Cbaa(config_from_dict(paper), 0) for _ in range(2)]
+    for k, h in enumerate(hs):
+        h.reset()
+        sel = part == k
+        h.update(torch.from_numpy(w.src[sel].view(np.int32)).cuda(), torch.from_numpy(w.dst[sel].view(np.int32)).cuda())
+    csb = hs[0].nbytes // 16
+    hs[0].merge_slice_zc([hs[1].cube_ptr() + lo * csb], lo, hi)
+    h1, s1, rc1 = hs[0].detect(1024, cs_lo=lo, cs_hi=hi)
+    h2, s2, rc2 = hs[0].detect(1024, cs_lo=lo, cs_hi=hi)
+    torch.cuda.synchronize()
+    ref, _ = O.update(paper, w.src, w.dst)
+    assert np.array_equal(hs[0].cube().cpu().numpy()[lo * csb: hi * csb], ref[lo * csb: hi * csb])
+    st, oh, ostats = O.detect(paper, ref, 1024)
+    oh = oh[(oh["cs"] >= lo) & (oh["cs"] < hi)]
+    assert_stats_equal(s1, ostats[lo:hi])
+    assert_hosts_equal(h1, oh)
+    assert_stats_equal(s2, ostats[lo:hi])
+    assert_hosts_equal(h2, oh)
