@@ -588,6 +588,11 @@ def main():
     algo_in = 8 * n                       # §8(d): 8 B of input per pair
     algo_bits = 4 * n                     # §8(d): |RA|+|VA| = 4 single-bit ORs per pair
     nb = ncu_binned()
+
+    def ncu_per_pair(key):
+        u, m = nb.get("update") or {}, nb.get("pairs_per_update")
+        return u[key] / m if (key in u and m) else None
+
     update_block = {
         "update_ms": upd, "pairs": n,
         "input_hbm": {"achieved_gbs": algo_in / (upd / 1e3) / 1e9, "peak_gbs": hbm,
@@ -595,15 +600,18 @@ def main():
                       "note": "8 B/pair input stream over the whole update (all kernels), SURVEY 8(d)"},
         "l2_red": {"algorithmic_bitsets_per_s": algo_bits / (upd / 1e3), "red_peak_per_s": red_peak,
                    "frac": (algo_bits / (upd / 1e3) / red_peak) if red_peak else None,
-                   "issued_l2_reds_per_update": (nb.get("update") or {}).get("l2_red_requests"),
-                   "issued_l2_red_sectors_per_update": (nb.get("update") or {}).get("l2_red_sectors"),
+                   "issued_l2_reds_per_update": (ncu_per_pair("l2_red_requests") or 0) * n or None,
+                   "issued_l2_reds_per_pair": ncu_per_pair("l2_red_requests"),
+                   "issued_l2_red_sectors_per_update": (ncu_per_pair("l2_red_sectors") or 0) * n or None,
                    "note": "4 bit-sets/pair / update time vs tools/redbench --quick RED.OR peak (random unique "
                            "words, 64 MiB L2-resident) measured in this run; > 1 means the design sets more "
                            "bits per second than one L2 RED each could (binned: ORs done in shared memory)"},
-        "dram": {"bytes_per_update": (nb.get("update") or {}).get("dram_bytes"),
+        # ncu bytes/REDs come from one 100M-pair C2 update: scaled per pair to this run's update
+        "dram": {"bytes_per_update": ncu_per_pair("dram_bytes") * n if ncu_per_pair("dram_bytes") else None,
                  "algorithmic_bytes": algo_in,
-                 "ratio": ((nb.get("update") or {}).get("dram_bytes") or 0) / algo_in if nb.get("update") else None,
-                 "source": os.path.relpath(NCU_BINNED, ROOT)},
+                 "ratio": ncu_per_pair("dram_bytes") / 8 if ncu_per_pair("dram_bytes") else None,
+                 "source": os.path.relpath(NCU_BINNED, ROOT) + f" ({nb.get('pairs_per_update')} pairs per captured "
+                           "update, scaled per pair)"},
     }
     plan_s = lat_handle.update_plan(int(per_call_pairs))
     if plan_s.startswith("binned"):
@@ -620,9 +628,10 @@ def main():
         roofline = {"kernel": scat, "bound": "hbm",
                     "achieved": 8 * per_call_pairs / (tsc / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": 8 * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,
-                    "traffic": (nb.get(scat) or {}).get("dram_bytes_per_launch"),
+                    "traffic": ((nb.get(scat) or {}).get("dram_bytes_per_launch", 0) / nb["pairs_per_update"]
+                                * per_call_pairs) if (nb.get(scat) and nb.get("pairs_per_update")) else None,
                     "traffic_source": os.path.relpath(NCU_BINNED, ROOT) + " (ncu --set full, dram__bytes_read+write "
-                                      "per launch)",
+                                      "of the captured launch, scaled to this launch's pairs)",
                     "algorithmic": "SURVEY 8(d): 8 B/pair of input read per launch (pairs per launch x 8 B)",
                     "design_bytes_per_pair": design,
                     "design_frac": design * per_call_pairs / (tsc / 1e3) / 1e9 / hbm,

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_count(const __grid_consta
 // the cube is exact for any input — the sample only decides how much of the work takes the fast path.
 constexpr uint32_t kSampleUnit = 8;                // pairs per sample unit (one sector per array)
 constexpr int kSampleUnroll = 2;
+template <bool PREFIX>
 __global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_constant__ Geo G, const __grid_constant__ BinGeo B,
                                                             const uint32_t* __restrict__ src,
                                                             const uint32_t* __restrict__ dst, uint64_t n,
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kCountThreads) k_bin_sample(const __grid_const
 #pragma unroll
       for (uint32_t e = 0; e < kSampleUnit; ++e) {
         uint32_t bin, ent;
-        if (e < cnt[v] && pair_bin<false>(G, B, ss[v][e], dd[v][e], bin, ent)) atomicAdd(&hist[bin], 1u);
+        if (e < cnt[v] && pair_bin<PREFIX>(G, B, ss[v][e], dd[v][e], bin, ent)) atomicAdd(&hist[bin], 1u);
       }
   }
   __syncthreads();
@@ -600,15 +601,21 @@ constexpr int kWRankBits = 14;
 constexpr int kWApplyThreads = CBAA_WAPPLY_THREADS;
 constexpr uint64_t kWEntMask = (1ull << 48) - 1;   // staged entry: bin << 48 | LP << 6 | row mod 64
 constexpr size_t kWScatterSmem = (size_t)kBinTile * 8 + (3 * kWBins + 1) * 4;   // 76 KiB: two CTAs per SM
+constexpr size_t kWScatterSmemPrefix = kWScatterSmem + 4096 * 4;                // + the a0 class table
 constexpr size_t kWApplySmem = 2 * 16384 * 4;                                   // two word groups, 128 KiB
 
+// PREFIX: raw on-wire pairs, classified by the inner prefixes (a0) with the two 8 KiB bitmaps
+// staged in shared memory; pairs with zero or two inner endpoints are skipped and counted here (every
+// pair passes through this kernel, so the bin regions can still come from a sample).
+template <bool PREFIX>
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(const __grid_constant__ Geo G,
                                                              const uint32_t* __restrict__ src,
                                                              const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
                                                              int vec, uint32_t* __restrict__ cursor,
                                                              uint64_t* __restrict__ entries,
                                                              const uint32_t* __restrict__ start,
-                                                             uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e) {
+                                                             uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e,
+                                                             unsigned long long* __restrict__ skipped) {
   constexpr uint32_t nbins = kWBins;
   constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread
   constexpr uint32_t wchunk = kPerLane * 32;              // 128 bins per warp
@@ -617,11 +624,30 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
   uint32_t* base = reinterpret_cast<uint32_t*>(stage + kBinTile);   // [nbins] this tile's slot base
   uint32_t* toff = base + nbins;                          // [nbins + 1] tile counts → exclusive offsets
   uint32_t* rend = toff + nbins + 1;                      // [nbins] region ends start[b + 1]
+  uint32_t* scode = rend + nbins;                         // PREFIX: [4096] 2-bit class of every /16
   __shared__ uint32_t s_w[kBinThreads / 32];
   __shared__ int s_ovf;
   const uint32_t tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   for (uint32_t b = tid; b < nbins; b += kBinThreads) toff[b] = 0, rend[b] = start[b + 1];
+  // the two /16 bitmaps of is_inner folded into one 2-bit code per /16 (0 outer, 1 inner, 2 exact check):
+  // one shared-memory load per endpoint
+  if (PREFIX)
+    for (uint32_t j = tid; j < 4096; j += kBinThreads) {
+      const uint32_t f = (G.full_bits[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      const uint32_t q = (G.part_bits[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      uint32_t c = 0;
+      for (uint32_t e = 0; e < 16; ++e) c |= (((f >> e) & 1u) ? 1u : ((q >> e) & 1u) ? 2u : 0u) << (2 * e);
+      scode[j] = c;
+    }
+  uint32_t skip = 0;
+  auto inner = [&](uint32_t ip) {   // is_inner with the classes in shared memory
+    const uint32_t t = ip >> 16, c = (scode[t >> 4] >> ((t & 15) << 1)) & 3u;
+    if (c != 2u) return c == 1u;
+    bool in = false;
+    for (uint32_t k = 0; k < G.n_prefix; ++k) in |= (ip & G.pmask[k]) == G.prefix[k];
+    return in;
+  };
   if (tid == 0) s_ovf = 0;
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), toff_sa = pin(smem_addr(toff));
@@ -649,11 +675,19 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
     }
 #pragma unroll
     for (int i = 0; i < kBinPPT; ++i) {
-      const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;           // P:175, Q2
+      bool ok = whole || t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3) < c1;
+      uint32_t iip = key[i], oip = ent[i];
+      if (PREFIX) {   // a0: keep inner→outer, swap outer→inner, skip the rest (Q25); branch-free
+        const bool si = inner(iip), di = inner(oip);
+        skip += (ok && si == di) ? 1u : 0u;
+        ok = ok && si != di;
+        iip = di ? ent[i] : key[i];
+        oip = di ? key[i] : ent[i];
+      }
+      const uint32_t mi = pa * iip + pb, mo = pa * oip + pb;                 // P:175, Q2
       const uint32_t row = mix32(mo ^ pbv) & 4095u;                         // P:230 (g = 4096)
       const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                  // (cs, row >> 6), r = 4
       ent[i] = mi >> 4;                                                     // LP
-      const bool ok = whole || t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3) < c1;
       key[i] = ok ? ((row & 63u) << 24) | (bin << kWRankBits) | atoms_inc(toff_sa + 4u * bin) : 0xffffffffu;
     }
     __syncthreads();
@@ -728,6 +762,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
     for (int j = 0; j < (int)kPerLane; ++j) toff[w0 + 32 * j + lane] = 0;
     if (tid == 0) s_ovf = 0;
     __syncthreads();
+  }
+  if (PREFIX && skipped) {   // (null: an exact count already counted them)
+    skip = warp_sum(skip);
+    if (lane == 0 && skip) atomicAdd(skipped, (unsigned long long)skip);
   }
 }
 

@@ -454,12 +454,13 @@ void t_end(cbaa_handle* h, int k, cudaStream_t s) {
 int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t kChunk = h->bin_chunk;
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-  const bool wide = h->bin_wide && !prefix && !h->bin_wc;   // 64-bit entries, 1024 bins
+  const bool wide = h->bin_wide && !h->bin_wc;   // 64-bit entries, 1024 bins
   const BinGeo& B = wide ? h->BW : h->B;
   // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
   const uint32_t slack = h->bin_wc ? 8u * (uint32_t)h->sms : 0u;
   // sampled region sizing (k_bin_sample): normalised input, tile scatter, chunks of ≥ bin_sample_min pairs
-  const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
+  // (prefix mode: only on the wide path, whose scatter counts the skipped pairs itself)
+  const uint32_t samp = ((!prefix || wide) && !h->bin_wc) ? h->bin_sample_log2 : 0u;
   const uint64_t mx = std::min(n, kChunk);
   const bool any_sampled = samp && mx >= h->bin_sample_min;
   // Σ cap(b) ≤ exact: m + nbins·(slack + 7); sampled (Σ est ≤ m + 2^L, Cauchy-Schwarz on the √ terms):
@@ -507,8 +508,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     const uint64_t per_c = (((m + nc - 1) / nc) + 3) & ~3ull;
     const uint32_t sl = samp && m >= h->bin_sample_min ? samp : 0u;
     int tk = t_begin(h, 0, s);
-    if (sl)
-      k_bin_sample<<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
+    if (sl && prefix)
+      k_bin_sample<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
+    else if (sl)
+      k_bin_sample<false><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
     else if (prefix)
       k_bin_count<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, h->skipped);
     else
@@ -522,9 +525,13 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     if ((rc = launch_check(h, "k_bin_starts"))) return rc;
     tk = t_begin(h, 2, s);
     if (wide) {
-      k_bin_scatter_w<<<B.nblk, kBinThreads, kWScatterSmem, s>>>(h->G, a, b, m, per, vec, cursor,
-                                                                 (uint64_t*)h->bin_ent, start, log_n,
-                                                                 (uint64_t*)h->bin_log);
+      if (prefix)
+        k_bin_scatter_w<true><<<B.nblk, kBinThreads, kWScatterSmemPrefix, s>>>(
+            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log,
+            sl ? h->skipped : nullptr);
+      else
+        k_bin_scatter_w<false><<<B.nblk, kBinThreads, kWScatterSmem, s>>>(
+            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log, nullptr);
     } else if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
       const uint32_t nw = (uint32_t)h->sms;
       const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
@@ -737,7 +744,8 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
     if (h->binnable) {
       const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((3 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
-      cudaFuncSetAttribute(k_bin_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      cudaFuncSetAttribute(k_bin_sample<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      cudaFuncSetAttribute(k_bin_sample<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
       const char* sp = std::getenv("CBAA_BIN_SAMPLE");
       if (sp) {
         const unsigned long v = std::strtoul(sp, nullptr, 10);
@@ -776,8 +784,10 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
         W.nbins = h->G.n_cs << 6;
         W.nblk = B.nblk;
         W.ncols = B.ncols;
-        cudaFuncSetAttribute(k_bin_scatter_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmem);
-        cudaFuncSetAttribute(k_bin_scatter_w, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_bin_scatter_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmem);
+        cudaFuncSetAttribute(k_bin_scatter_w<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_bin_scatter_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmemPrefix);
+        cudaFuncSetAttribute(k_bin_scatter_w<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_bin_apply_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
       }
       cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
@@ -1494,8 +1504,8 @@ int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t bufle
   std::string p;
   if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min) {
     const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-    const bool wide = h->bin_wide && !prefix && !h->bin_wc;
-    const uint32_t samp = (!prefix && !h->bin_wc) ? h->bin_sample_log2 : 0u;
+    const bool wide = h->bin_wide && !h->bin_wc;
+    const uint32_t samp = ((!prefix || wide) && !h->bin_wc) ? h->bin_sample_log2 : 0u;
     const bool sampled = samp && std::min(n, h->bin_chunk) >= h->bin_sample_min;
     p = std::string(wide ? "binned-wide " : "binned ") + (sampled ? "k_bin_sample" : "k_bin_count") + " k_bin_starts " +
         (wide ? "k_bin_scatter_w" : h->bin_wc ? "k_bin_wc" : "k_bin_scatter") + " " +

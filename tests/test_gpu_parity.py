@@ -562,6 +562,32 @@ def test_binned_inner_prefix(paper):
     assert cb.skipped() == skipped >= 1000
 
 
+@pytest.mark.parametrize("sample", ["9", "14"])
+def test_binned_inner_prefix_sampled(paper, sample, monkeypatch):
+    """a0 on the wide path with sampled bin regions (forced on a small window): the sample classifies, the
+    scatter classifies and counts the skips (once), regions that fall short spill to the overflow log;
+    prefixes mix /16s (full bitmap) with a /24 and a /20 (partial bitmap, exact comparison)."""
+    monkeypatch.setenv("CBAA_BIN_SAMPLE_MIN", "1")
+    monkeypatch.setenv("CBAA_BIN_SAMPLE", sample)
+    spec = W.WindowSpec(n=400_000, n_hosts=6000, n_flows=60000, victims=(3000,), scanners=(2500,))
+    w = W.generate(spec, 14)
+    extra = [(0xC0A80100, 0xFFFFFF00), (0x0AB00000, 0xFFF00000)]   # 192.168.1.0/24, 10.176.0.0/12-ish /20
+    q = dict(paper, direction=1, prefixes=w.prefixes[:14] + extra, **BIN)
+    junk_s, junk_d = W.random_pairs(20_000, 9)
+    rng = np.random.default_rng(3)
+    sub24 = (0xC0A80100 | rng.integers(0, 256, 5000)).astype(np.uint32)     # inner via the /24
+    out24 = (0xC0A80200 | rng.integers(0, 256, 5000)).astype(np.uint32)     # same /16, outside the /24
+    raw_s = np.concatenate([w.raw_src, junk_s, out24, sub24])
+    raw_d = np.concatenate([w.raw_dst, junk_d, sub24, out24])
+    cb = handle(q)
+    cb.reset()
+    cb.update(dev(raw_s), dev(raw_d))
+    ref, skipped = O.update(q, raw_s, raw_d)
+    assert np.array_equal(gpu_cube(cb), ref)
+    assert cb.skipped() == skipped > 0
+    assert cb.update_plan(len(raw_s)).startswith("binned-wide k_bin_sample")
+
+
 def test_binned_chunks_and_accumulate(paper, monkeypatch):
     """Several count/scatter/apply rounds per call (small CBAA_BIN_CHUNK) and across calls, OR-ed into a
     cube that already holds bits from the direct kernel."""
