@@ -734,16 +734,29 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
       if (tid == 0) toff[nbins] = tot;
     }
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kBinPPT; ++i) {
-      if (key[i] == 0xffffffffu) continue;
+    auto stage_one = [&](int i) {
       const uint32_t bin = (key[i] >> kWRankBits) & (nbins - 1u);
       const uint32_t pos = toff[bin] + (key[i] & ((1u << kWRankBits) - 1u));
       stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | (key[i] >> 24);
+    };
+    if (!PREFIX && whole) {   // every pair of the tile is valid: no per-pair test (no reconvergence)
+#pragma unroll
+      for (int i = 0; i < kBinPPT; ++i) stage_one(i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kBinPPT; ++i)
+        if (key[i] != 0xffffffffu) stage_one(i);
     }
     __syncthreads();
     const uint32_t total = toff[nbins];
-    if (!s_ovf) {
+    if (!s_ovf && total == kBinTile) {   // a full tile: compile-time trip count, no bounds tests
+#pragma unroll 8
+      for (int k = 0; k < kBinTile / kBinThreads; ++k) {
+        const uint32_t p = tid + k * kBinThreads;
+        const uint64_t v = stage[p];
+        entries[base[(uint32_t)(v >> 48)] + p] = v & kWEntMask;
+      }
+    } else if (!s_ovf) {
 #pragma unroll 4
       for (uint32_t p = tid; p < total; p += kBinThreads) {
         const uint64_t v = stage[p];
