@@ -72,6 +72,13 @@ __device__ __forceinline__ uint32_t atoms_inc(uint32_t a) {
   asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(a));
   return v;
 }
+// Predicated fetch-and-increment (one instruction, no branch): returns 0 when pred == 0.
+__device__ __forceinline__ uint32_t atoms_inc_if(uint32_t a, uint32_t pred) {
+  uint32_t v = 0;
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p atom.shared.add.u32 %0, [%1], 1;\n}"
+               : "+r"(v) : "r"(a), "r"(pred));
+  return v;
+}
 // Opaque to the optimizer: keeps a loop-invariant in a register instead of re-reading the parameter bank.
 __device__ __forceinline__ uint32_t pin(uint32_t x) {
   asm volatile("" : "+r"(x));
@@ -673,22 +680,34 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
         ent[i] = k < c1 ? __ldcs(dst + k) : 0u;
       }
     }
+    if (!PREFIX && whole) {   // every pair valid: unconditional rank (no branch around each ATOMS)
 #pragma unroll
-    for (int i = 0; i < kBinPPT; ++i) {
-      bool ok = whole || t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3) < c1;
-      uint32_t iip = key[i], oip = ent[i];
-      if (PREFIX) {   // a0: keep inner→outer, swap outer→inner, skip the rest (Q25); branch-free
-        const bool si = inner(iip), di = inner(oip);
-        skip += (ok && si == di) ? 1u : 0u;
-        ok = ok && si != di;
-        iip = di ? ent[i] : key[i];
-        oip = di ? key[i] : ent[i];
+      for (int i = 0; i < kBinPPT; ++i) {
+        const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;         // P:175, Q2
+        const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
+        const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                // (cs, row >> 6), r = 4
+        ent[i] = mi >> 4;                                                   // LP
+        key[i] = ((row & 63u) << 24) | (bin << kWRankBits) | atoms_inc(toff_sa + 4u * bin);
       }
-      const uint32_t mi = pa * iip + pb, mo = pa * oip + pb;                 // P:175, Q2
-      const uint32_t row = mix32(mo ^ pbv) & 4095u;                         // P:230 (g = 4096)
-      const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                  // (cs, row >> 6), r = 4
-      ent[i] = mi >> 4;                                                     // LP
-      key[i] = ok ? ((row & 63u) << 24) | (bin << kWRankBits) | atoms_inc(toff_sa + 4u * bin) : 0xffffffffu;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kBinPPT; ++i) {
+        bool ok = whole || t0 + 4ull * ((uint64_t)(i >> 2) * kBinThreads + tid) + (i & 3) < c1;
+        uint32_t iip = key[i], oip = ent[i];
+        if (PREFIX) {   // a0: keep inner→outer, swap outer→inner, skip the rest (Q25); branch-free
+          const bool si = inner(iip), di = inner(oip);
+          skip += (ok && si == di) ? 1u : 0u;
+          ok = ok && si != di;
+          iip = di ? ent[i] : key[i];
+          oip = di ? key[i] : ent[i];
+        }
+        const uint32_t mi = pa * iip + pb, mo = pa * oip + pb;               // P:175, Q2
+        const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
+        const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                // (cs, row >> 6), r = 4
+        ent[i] = mi >> 4;                                                   // LP
+        const uint32_t rank = atoms_inc_if(toff_sa + 4u * bin, ok ? 1u : 0u);
+        key[i] = ok ? ((row & 63u) << 24) | (bin << kWRankBits) | rank : 0xffffffffu;
+      }
     }
     __syncthreads();
     // per-bin reservation and offsets (rotated lane ownership as in k_bin_scatter)

@@ -34,12 +34,18 @@ def _hosts_equal(gh, oh):
     return True
 
 
+def _same_status(rc, st):
+    """Library status (0, CBAA_E_TUPLE_CAP = -6, CBAA_E_CAPACITY = -5) vs the oracle's (0, 1 overflow, 2 capacity)."""
+    return {0: 0, -6: 1, -5: 2}.get(rc, rc) == st
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=500_000_000)
     ap.add_argument("--seed", type=int, default=5)
     ap.add_argument("--detects", type=int, default=200)
     ap.add_argument("--max-cube-mib", type=int, default=512)
+    ap.add_argument("--r", type=int, default=None, help="only geometries with this r")
     args = ap.parse_args()
     import torch
 
@@ -58,6 +64,8 @@ def main():
     src = torch.from_numpy(w.src.view(np.int32)).cuda()
     dst = torch.from_numpy(w.dst.view(np.int32)).cuda()
     for geo in W.c5_geometries():
+        if args.r is not None and geo["r"] != args.r:
+            continue
         p = dict(O.default_params(), **geo)
         cb = Cbaa(config_from_dict(p), 0)
         times = []
@@ -91,7 +99,7 @@ def main():
             host_parity = None
             if ref is not None and sum(min(s["tuples"], p["tuple_cap"]) for s in stats) <= (1 << 26):
                 st, oh, _ = O.detect(p, ref, theta, cap=1 << 22)
-                host_parity = bool(st == rc and _hosts_equal(hosts, oh))
+                host_parity = bool(_same_status(rc, st) and _hosts_equal(hosts, oh))
             m = truth.score(hosts["ip"].tolist(), tc, theta)
             print(json.dumps({"r": p["r"], "g": p["g"], "cbn": p["cbn"][0], "theta": theta,
                               "cube_mib": cb.nbytes >> 20, "update_ms": round(upd, 4),
@@ -104,7 +112,7 @@ def main():
                               "overflow_cs": int(sum(s["overflow"] for s in stats)),
                               "lambda_over_theta": round(lam / theta, 3), "overloaded": lam > theta / 4,
                               "truth_H": m["H"], "fnr": m["fnr"], "fpr": m["fpr"], "ftr": m["ftr"],
-                              "cube_parity_whole_window": cube_parity, "host_parity": host_parity,
+                              "status": rc, "cube_parity_whole_window": cube_parity, "host_parity": host_parity,
                               "oracle_update_s": round(oracle_s, 1) if ref is not None else None}), flush=True)
         cb.close()
         del ref

@@ -60,7 +60,7 @@ def test_reduced_c5_sweep(paper, c5_small, r, g, cbn):
     for theta in THETAS:
         hosts, stats, rc = cb.detect(theta, cap=1 << 22)
         st, oh, ostats = O.detect(p, ref, theta, cap=1 << 22)
-        assert rc == st
+        assert {0: 0, -6: 1, -5: 2}.get(rc, rc) == st   # library vs oracle status codes
         assert_stats_equal(stats, ostats)
         assert_hosts_equal(hosts, oh)
         m = truth.score(hosts["ip"].tolist(), tc, theta)

@@ -9,6 +9,8 @@
 #   sanitize  compute-sanitizer memcheck/racecheck/synccheck/initcheck of tools/sanitize.py
 #   sweep     tests/sweep_c5.py (C5 accuracy/throughput sweep)
 #   c4full    tests/full_c4.py (config 4 at full size)
+#   func2     functional N = 2 runs on ONE GPU (gloo process group, IPC exchange with device barriers):
+#             C2 pipelined, C3, C4 — their times are meaningless (two ranks share the GPU)
 set -x
 T=$1; shift
 for S in "$@"; do
@@ -32,6 +34,10 @@ for S in "$@"; do
       done ;;
     sweep) timeout 2400 python -m tests.sweep_c5 > gpurun_out/sweep_c5_$T.jsonl 2> gpurun_out/sweep_c5_$T.err; tail -2 gpurun_out/sweep_c5_$T.err ;;
     c4full) timeout 2400 python -m tests.full_c4 > gpurun_out/full_c4_$T.jsonl 2> gpurun_out/full_c4_$T.err; tail -2 gpurun_out/full_c4_$T.jsonl ;;
+    func2)
+      for W in C2 C3 C4; do
+        CBAA_BENCH_BACKEND=gloo timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --workload $W --steps 3 --warmup 3 --no-e2e --detect-samples 5 > gpurun_out/bench_n2func_${W}_$T.json 2> gpurun_out/bench_n2func_${W}_$T.err; echo "func2 $W rc=$?"; tail -c 400 gpurun_out/bench_n2func_${W}_$T.json
+      done ;;
     *) echo "unknown stage $S" ;;
   esac
 done
