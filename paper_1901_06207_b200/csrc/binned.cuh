@@ -601,7 +601,8 @@ __device__ __forceinline__ void reds_or_if_clear(uint32_t a, uint32_t bit, uint3
 // (no separate bin array).  The apply gives each bin one CTA with a 128 KiB image of its two word groups.
 // DRAM: 8 instead of 4 B written and read back per pair.
 constexpr int kWBins = 1024;                   // 2^4 CSs × 4096 / 64 rows
-constexpr int kWRankBits = 14;
+// rank key of a pair: cs << 28 | row << 16 | rank in the tile (< 2^13), so key >> 22 is the bin
+// (cs << 6 | row >> 6) and (key >> 16) mod 64 the row bits kept in the entry; 0xffffffff = no pair
 #ifndef CBAA_WAPPLY_THREADS
 #define CBAA_WAPPLY_THREADS 1024
 #endif
@@ -685,9 +686,9 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
       for (int i = 0; i < kBinPPT; ++i) {
         const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;         // P:175, Q2
         const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
-        const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                // (cs, row >> 6), r = 4
+        const uint32_t hi = (mi << 28) | (row << 16);                       // r = 4: cs = mi mod 16
         ent[i] = mi >> 4;                                                   // LP
-        key[i] = ((row & 63u) << 24) | (bin << kWRankBits) | atoms_inc(toff_sa + 4u * bin);
+        key[i] = hi | atoms_inc(toff_sa + 4u * (hi >> 22));                 // bin (cs, row >> 6)
       }
     } else {
 #pragma unroll
@@ -703,10 +704,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
         }
         const uint32_t mi = pa * iip + pb, mo = pa * oip + pb;               // P:175, Q2
         const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
-        const uint32_t bin = ((mi & 15u) << 6) | (row >> 6);                // (cs, row >> 6), r = 4
+        const uint32_t hi = (mi << 28) | (row << 16);                       // r = 4: cs = mi mod 16
         ent[i] = mi >> 4;                                                   // LP
-        const uint32_t rank = atoms_inc_if(toff_sa + 4u * bin, ok ? 1u : 0u);
-        key[i] = ok ? ((row & 63u) << 24) | (bin << kWRankBits) | rank : 0xffffffffu;
+        const uint32_t rank = atoms_inc_if(toff_sa + 4u * (hi >> 22), ok ? 1u : 0u);
+        key[i] = ok ? hi | rank : 0xffffffffu;
       }
     }
     __syncthreads();
@@ -754,9 +755,9 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
     }
     __syncthreads();
     auto stage_one = [&](int i) {
-      const uint32_t bin = (key[i] >> kWRankBits) & (nbins - 1u);
-      const uint32_t pos = toff[bin] + (key[i] & ((1u << kWRankBits) - 1u));
-      stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | (key[i] >> 24);
+      const uint32_t bin = key[i] >> 22;
+      const uint32_t pos = toff[bin] + (key[i] & 0xffffu);
+      stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | ((key[i] >> 16) & 63u);
     };
     if (!PREFIX && whole) {   // every pair of the tile is valid: no per-pair test (no reconvergence)
 #pragma unroll
