@@ -426,8 +426,7 @@ def main():
     def launches():
         return sum(c.kernel_launches for c in cbs)
 
-    pipelined = (not args.no_pipeline and args.workload in ("C1", "C2") and args.update_mode == "binned"
-                 and (world == 1 or exchange == "ipc"))
+    pipelined = not args.no_pipeline and args.update_mode == "binned" and (world == 1 or exchange == "ipc")
     if not pipelined:
         with torch.cuda.stream(stream):
             for _ in range(max(args.warmup, 3)):   # at least 3 untimed warm-up windows
@@ -463,16 +462,16 @@ def main():
     else:
         # the object tests/test_gpu_measured.py checks against the oracle window by window
         pipe = WindowPipeline(cfg, local, THETA, rank=rank, world=world, update_stream=stream,
-                              gather=lambda h: D.gather_hosts(h, rank, world))
+                              gather=lambda h: D.gather_hosts(h, rank, world),
+                              routers=len(dev_blocks) if plan.per_router_cube else 1)
         if world > 1:
             pipe.set_exchanges([D.IpcExchange(c, rank, world) for c in pipe.cbs])
-        s0, d0 = dev_blocks[0]
         for _ in range(max(args.warmup, 3)):
-            pipe.submit(s0, d0)
+            pipe.submit(dev_blocks)
         pipe.flush()
         torch.cuda.synchronize()
         launches0 = pipe.kernel_launches
-        for c in pipe.cbs:
+        for c in pipe.handles:
             c.set_phase_timing(True)
         pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
         t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -482,7 +481,7 @@ def main():
         with ClockSampler(local) as clk:
             t_start.record(pipe.s_upd)
             for k in range(args.steps):
-                pipe.submit(s0, d0, pevs[k])
+                pipe.submit(dev_blocks, events=pevs[k])
             hosts = pipe.flush()
             t_end.record(pipe.s_det)
             torch.cuda.synchronize()
@@ -490,7 +489,7 @@ def main():
             dist.barrier()
         nlaunch = pipe.kernel_launches - launches0
         phase_ms, phase_calls = [0.0] * 4, 0
-        for c in pipe.cbs:
+        for c in pipe.handles:
             m, k_ = c.update_phase_ms()
             phase_ms = [a + b for a, b in zip(phase_ms, m)]
             phase_calls += k_
@@ -500,15 +499,19 @@ def main():
         # the detect-latency samples below run on a window of the measured configuration
         lat_handle = pipe.cbs[0]
         with torch.cuda.stream(stream):
-            lat_handle.reset(stream)
-            lat_handle.update(s0, d0, stream)
+            st0 = pipe.sets[0]
+            for j, (s_, d_) in enumerate(dev_blocks):
+                st0[j if plan.per_router_cube else 0].update(s_, d_, stream)
+            if len(st0) > 1:
+                st0[0].merge(st0[1:], stream)
         if world > 1:
             for px in pipe.exchanges:
                 px.close()
             with torch.cuda.stream(stream):
                 window()                  # N > 1: the latency below includes the exchange on this cube
             lat_handle = cb
-        schedule = "pipelined: detect(k) + reset on a high-priority stream beside update(k+1), two cubes"
+        schedule = ("pipelined: [merge of the router cubes,] detect(k) + reset on a high-priority stream beside "
+                    "update(k+1), two cube sets")
     if world > 1:
         elapsed_ms = _allreduce(elapsed_ms, dist.ReduceOp.MAX)
 

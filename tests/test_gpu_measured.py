@@ -31,9 +31,10 @@ def test_bench_pipeline_matches_oracle(paper):
     n = (1 << 24) + 12345
     wins = [_window(s, n) for s in (11, 12, 13)]
     pipe = WindowPipeline(config_from_dict(paper), 0, 1024, with_stats=True)
-    got = []
+    got, keep = [], []   # device inputs stay referenced until the pipeline's streams are done
     for w in wins:
-        out = pipe.submit(dev(w.src), dev(w.dst))
+        keep.append((dev(w.src), dev(w.dst)))
+        out = pipe.submit(*keep[-1])
         if out is not None:
             got.append((out, pipe.last_stats))
     got.append((pipe.flush(), pipe.last_stats))
@@ -110,5 +111,32 @@ def test_theta_change_reuses_graph(paper):
     for theta in (1024, 256, 1024, 4096, 1500, 1500):
         hosts, stats, rc = cb.detect(theta)
         st, oh, ostats = O.detect(paper, ref, theta)
+        assert_stats_equal(stats, ostats)
+        assert_hosts_equal(hosts, oh)
+
+
+def test_pipeline_router_sets_match_oracle(paper):
+    """Config 3's pipelined schedule: each window is 3 router streams into 3 router cubes, OR-merged on
+    the update stream and detected beside the next window's updates; every window's hosts and
+    stats == the oracle of the routers' concatenated streams."""
+    from paper_1901_06207_b200.cbaa import config_from_dict
+    from paper_1901_06207_b200.pipeline import WindowPipeline
+
+    spec = W.WindowSpec(n=2_000_003, n_hosts=40_000, n_flows=300_000, scanners=(1500, 2500, 5000))
+    wins = [[W.generate(spec, 31 + k, packet_seed=100 * k + r, with_raw=False) for r in range(3)] for k in range(3)]
+    pipe = WindowPipeline(config_from_dict(paper), 0, 1024, with_stats=True, routers=3)
+    got, keep = [], []
+    for routers in wins:
+        keep.append([(dev(w.src), dev(w.dst)) for w in routers])
+        out = pipe.submit(keep[-1])
+        if out is not None:
+            got.append((out, pipe.last_stats))
+    got.append((pipe.flush(), pipe.last_stats))
+    torch.cuda.synchronize()
+    for routers, (hosts, stats) in zip(wins, got):
+        src = np.concatenate([w.src for w in routers])
+        dst = np.concatenate([w.dst for w in routers])
+        ref = O.update_parallel(paper, src, dst)
+        st, oh, ostats = O.detect(paper, ref, 1024)
         assert_stats_equal(stats, ostats)
         assert_hosts_equal(hosts, oh)
