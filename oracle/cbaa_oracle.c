@@ -556,3 +556,74 @@ uint64_t orc_lp_roundtrip_failures(const orc_config* c, uint64_t lo, uint64_t hi
   }
   return fails;
 }
+
+/* ------------------------------------------------- sparse SketchFile "CBA2"
+ * The optional sparse/compressed form of the cross-router transfer (S:479
+ * "optionally sparse").  This build's format:
+ * the cube's bits are cut into blocks of 2^15 bits (4 KiB; bit 8j+k of the
+ * cube = bit k of byte j); a block is the ascending list of its set-bit
+ * positions p_0 < p_1 < …, written as the gaps p_0, p_1 − p_0 − 1, … in
+ * LEB128 (7 bits per byte, low group first, bit 7 = "more").  Plain per-bit
+ * loops: one call per block. */
+#define ORC_SPARSE_BLOCK_BITS 32768u
+
+static uint64_t orc_leb128_len(uint32_t v) {
+  uint64_t n = 1;
+  while (v >= 128) { v >>= 7; ++n; }
+  return n;
+}
+
+/* Bytes of block b's varint stream (the last block may be short: nbits). */
+uint64_t orc_sparse_block_bytes(const uint8_t* cube, uint64_t nbytes, uint64_t b) {
+  uint64_t first = b * ORC_SPARSE_BLOCK_BITS, end = first + ORC_SPARSE_BLOCK_BITS, bytes = 0;
+  if (end > nbytes * 8) end = nbytes * 8;
+  int64_t prev = -1;
+  for (uint64_t i = first; i < end; ++i) {
+    if ((cube[i >> 3] >> (i & 7)) & 1u) {
+      int64_t pos = (int64_t)(i - first);
+      bytes += orc_leb128_len((uint32_t)(pos - prev - 1));
+      prev = pos;
+    }
+  }
+  return bytes;
+}
+
+/* Writes block b's varint stream to out; returns the bytes written. */
+uint64_t orc_sparse_block_encode(const uint8_t* cube, uint64_t nbytes, uint64_t b, uint8_t* out) {
+  uint64_t first = b * ORC_SPARSE_BLOCK_BITS, end = first + ORC_SPARSE_BLOCK_BITS, k = 0;
+  if (end > nbytes * 8) end = nbytes * 8;
+  int64_t prev = -1;
+  for (uint64_t i = first; i < end; ++i) {
+    if ((cube[i >> 3] >> (i & 7)) & 1u) {
+      int64_t pos = (int64_t)(i - first);
+      uint32_t gap = (uint32_t)(pos - prev - 1);
+      while (gap >= 128) { out[k++] = (uint8_t)(0x80u | (gap & 0x7Fu)); gap >>= 7; }
+      out[k++] = (uint8_t)gap;
+      prev = pos;
+    }
+  }
+  return k;
+}
+
+/* ORs block b's set bits, read from len bytes at in, into cube; returns 0, or 1 on a malformed
+ * stream (a varint past the end, a position past the block). */
+int orc_sparse_block_decode(const uint8_t* in, uint64_t len, uint8_t* cube, uint64_t nbytes, uint64_t b) {
+  uint64_t first = b * ORC_SPARSE_BLOCK_BITS, k = 0;
+  int64_t prev = -1;
+  while (k < len) {
+    uint64_t gap = 0;
+    int shift = 0;
+    for (;;) {
+      if (k >= len || shift > 28) return 1;
+      uint8_t byte = in[k++];
+      gap |= (uint64_t)(byte & 0x7Fu) << shift;
+      shift += 7;
+      if (!(byte & 0x80u)) break;
+    }
+    int64_t pos = prev + 1 + (int64_t)gap;
+    if (pos >= (int64_t)ORC_SPARSE_BLOCK_BITS || first + (uint64_t)pos >= nbytes * 8) return 1;
+    cube[(first + pos) >> 3] |= (uint8_t)(1u << ((first + pos) & 7));
+    prev = pos;
+  }
+  return 0;
+}

@@ -124,6 +124,9 @@ def lib():
             "orc_corrected_estimate": (dbl, [dbl, dbl, dbl]),
             "orc_hot_threshold": (dbl, [dbl, dbl, dbl, C.c_int]),
             "orc_union_threshold": (dbl, [dbl, dbl, dbl]),
+            "orc_sparse_block_bytes": (u64, [C.c_void_p, u64, u64]),
+            "orc_sparse_block_encode": (u64, [C.c_void_p, u64, u64, C.c_void_p]),
+            "orc_sparse_block_decode": (C.c_int, [C.c_void_p, u64, C.c_void_p, u64, u64]),
             "orc_cs_load": (None, [cfg, C.c_void_p, u32, P(u64), P(dbl), P(dbl)]),
             "orc_zmax": (u32, [dbl, u32]),
             "orc_zero_counts_ra": (None, [cfg, C.c_void_p, C.c_void_p]),
@@ -364,3 +367,47 @@ def deserialize(data: bytes):
     p = dict(default_params(), r=r, num_ra=nra, num_va=nva, g=g, cbn=cbn, clbs=clbs, mangle_a=a, mangle_b=b,
              bv_seed=bv, va_seeds=vs)
     return p, np.frombuffer(data, dtype=np.uint8, offset=off).copy()
+
+# ----------------------------------------------------------------- sparse SketchFile "CBA2"
+SPARSE_BLOCK_BITS = 32768
+
+
+def sparse_block_bytes(cube: np.ndarray, b: int) -> int:
+    return lib().orc_sparse_block_bytes(_ptr(cube), cube.size, b)
+
+
+def sparse_block_encode(cube: np.ndarray, b: int) -> bytes:
+    buf = np.zeros(sparse_block_bytes(cube, b) + 1, np.uint8)
+    n = lib().orc_sparse_block_encode(_ptr(cube), cube.size, b, _ptr(buf))
+    return buf[:n].tobytes()
+
+
+def serialize_sparse(p, cube: np.ndarray) -> bytes:
+    """The sparse SketchFile: the CBA1 header with magic "CBA2" (its u64 = the dense cube
+    length), u32 block bits (2^15), u64 block count, (blocks + 1) × u64 byte offsets of the blocks' varint
+    streams, then the streams (each: LEB128 gaps between ascending set-bit positions of the block)."""
+    import struct
+    dense = serialize(p, cube[:0])
+    head = b"CBA2" + dense[4:-8] + struct.pack("<Q", cube.size)
+    nb = (cube.size * 8 + SPARSE_BLOCK_BITS - 1) // SPARSE_BLOCK_BITS
+    streams = [sparse_block_encode(cube, b) for b in range(nb)]
+    offs = [0]
+    for st in streams:
+        offs.append(offs[-1] + len(st))
+    head += struct.pack("<IQ", SPARSE_BLOCK_BITS, nb) + struct.pack("<" + "Q" * (nb + 1), *offs)
+    return head + b"".join(streams)
+
+
+def deserialize_sparse(data: bytes, nbytes: int, header_bytes: int) -> np.ndarray:
+    """The cube of a CBA2 file whose header (through the u64 dense length) is header_bytes long."""
+    import struct
+    bits, nb = struct.unpack_from("<IQ", data, header_bytes)
+    assert bits == SPARSE_BLOCK_BITS
+    offs = struct.unpack_from("<" + "Q" * (nb + 1), data, header_bytes + 12)
+    base = header_bytes + 12 + 8 * (nb + 1)
+    cube = np.zeros(nbytes, np.uint8)
+    payload = np.frombuffer(data, np.uint8, offset=base)
+    for b in range(nb):
+        seg = np.ascontiguousarray(payload[offs[b]:offs[b + 1]])
+        assert lib().orc_sparse_block_decode(_ptr(seg), seg.size, _ptr(cube), nbytes, b) == 0
+    return cube

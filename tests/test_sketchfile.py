@@ -116,3 +116,43 @@ def test_device_file_header_golden(paper, golden, name):
     want = _golden_headers(golden)[name]
     data = h.serialize()
     assert bytes(data[:len(want)]) == want and not data[len(want):].any()
+
+
+# ------------------------------------------------------------------ sparse SketchFile "CBA2"
+def _bits_cube(nbytes, positions):
+    c = np.zeros(nbytes, np.uint8)
+    for pos in positions:
+        c[pos >> 3] |= np.uint8(1 << (pos & 7))
+    return c
+
+
+def test_sparse_block_streams_golden(golden):
+    """The oracle's block encoding equals the hand-computed LEB128 gap streams (tests/golden)."""
+    g = {k: bytes(v[0]) for k, v in golden("sparse_blocks.txt").items()}
+    cube = _bits_cube(3 * 4096, [0, 1, 130, 32767] + [32768 + q for q in (5, 6, 127, 16384)])
+    assert O.sparse_block_encode(cube, 0) == g["block0"]
+    assert O.sparse_block_encode(cube, 1) == g["block1"]
+    assert O.sparse_block_encode(cube, 2) == b""
+
+
+@pytest.mark.parametrize("density", [0.0, 0.001, 0.034, 0.5, 1.0])
+def test_sparse_roundtrip_and_size(paper, density):
+    """CBA2 round trip is bit-identical; stream bytes == Σ LEB128 lengths of the gaps counted in numpy;
+    a ragged last block (cube not a multiple of 4 KiB)."""
+    p = dict(paper, r=2, g=64, cbn=[10, 10, 10, 6], clbs=[0, 10, 20])   # 2^2·(3·1024 + 64)·64/8 = 100352 B
+    assert O.validate(p)[0] == 0
+    n = O.cube_bytes(p)
+    rng = np.random.default_rng(7)
+    bits = rng.random(n * 8) < density
+    cube = np.packbits(bits, bitorder="little")
+    data = O.serialize_sparse(p, cube)
+    hb = len(O.serialize(p, cube[:0]))
+    assert data[:4] == b"CBA2"
+    assert np.array_equal(O.deserialize_sparse(data, n, hb), cube)
+    want = 0
+    for b0 in range(0, n * 8, 32768):
+        pos = np.nonzero(bits[b0:b0 + 32768])[0]
+        gaps = np.diff(np.concatenate([[-1], pos])) - 1
+        want += int(np.sum(1 + (gaps >= 128) + (gaps >= 1 << 14) + (gaps >= 1 << 21)))
+    nb = -(-n * 8 // 32768)
+    assert len(data) == hb + 12 + 8 * (nb + 1) + want
