@@ -273,6 +273,17 @@ uint64_t cbaa_sketch_bytes(const cbaa_handle* h);
  * Synchronizes stream (the cube is read after earlier work on it). */
 int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream);
 
+/* The optional sparse form ("optionally sparse"): the
+ * same header with magic "CBA2" (its u64 = the dense cube length), then u32
+ * block bits = 32768, u64 blocks = ⌈cube bits / 32768⌉, (blocks + 1) × u64 byte
+ * offsets of the blocks' streams (from 0, ascending), then the streams: a
+ * block's set-bit positions p0 < p1 < … as the gaps p0, p1 − p0 − 1, … in
+ * LEB128 (7 bits per byte, low group first, bit 7 = more).  Encoded on the
+ * device (two passes: stream sizes, then the streams); *n_written = file size
+ * (CBAA_E_CAPACITY with that size if cap is too small).  cbaa_sketch_config and
+ * cbaa_deserialize accept both forms.  Synchronizes stream. */
+int cbaa_serialize_sparse(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream);
+
 /* Parses a SketchFile header from HOST bytes into *out (other fields default).
  * No GPU needed.  CBAA_E_CONFIG with last-error-style text in err (errlen bytes)
  * names the bad field: magic, version, a geometry invariant, or the payload length. */

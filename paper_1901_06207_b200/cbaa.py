@@ -95,6 +95,7 @@ _SIGS = {
                                  C.c_void_p]),
     "cbaa_sketch_bytes": (C.c_uint64, [_h]),
     "cbaa_serialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
+    "cbaa_serialize_sparse": (C.c_int, [_h, C.c_void_p, C.c_uint64, _P(C.c_uint64), C.c_void_p]),
     "cbaa_sketch_config": (C.c_int, [C.c_void_p, C.c_uint64, _P(Config), C.c_char_p, C.c_uint64]),
     "cbaa_deserialize": (C.c_int, [_h, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]),
     "cbaa_ipc_export": (C.c_int, [_h, C.c_void_p]),
@@ -423,6 +424,16 @@ class Cbaa:
         w = C.c_uint64()
         self._check(lib().cbaa_serialize(self._h, out.ctypes.data_as(C.c_void_p), n, C.byref(w), _stream(stream)),
                     "cbaa_serialize")
+        return out
+
+    def serialize_sparse(self, stream=None) -> np.ndarray:
+        """The cube as a sparse SketchFile "CBA2" (cbaa_serialize_sparse), uint8 numpy array."""
+        w = C.c_uint64()
+        rc = lib().cbaa_serialize_sparse(self._h, None, 0, C.byref(w), _stream(stream))
+        self._check(rc, "cbaa_serialize_sparse", allow=(E_CAPACITY,))
+        out = np.empty(w.value, dtype=np.uint8)
+        self._check(lib().cbaa_serialize_sparse(self._h, out.ctypes.data_as(C.c_void_p), w.value, C.byref(w),
+                                                _stream(stream)), "cbaa_serialize_sparse")
         return out
 
     def deserialize(self, data, merge: bool = False, stream=None):

@@ -1257,7 +1257,7 @@ struct Reader {
 
 // Parses the header; on success *payload points at the cube bytes and *plen is their length.
 int parse_sketch(const void* in, uint64_t n, cbaa_config* out, const uint8_t** payload, uint64_t* plen,
-                 std::string* why) {
+                 std::string* why, bool* sparse = nullptr) {
   auto bad = [&](const std::string& m) {
     if (why) *why = m;
     return CBAA_E_CONFIG;
@@ -1266,7 +1266,9 @@ int parse_sketch(const void* in, uint64_t n, cbaa_config* out, const uint8_t** p
   Reader R{(const uint8_t*)in, (const uint8_t*)in + n};
   char magic[4];
   for (int k = 0; k < 4; ++k) magic[k] = (char)R.u8();
-  if (!R.ok || std::memcmp(magic, "CBA1", 4) != 0) return bad("magic: expected \"CBA1\"");
+  const bool sp = R.ok && std::memcmp(magic, "CBA2", 4) == 0;   // the sparse form
+  if (!R.ok || (!sp && std::memcmp(magic, "CBA1", 4) != 0)) return bad("magic: expected \"CBA1\" or \"CBA2\"");
+  if (sparse) *sparse = sp;
   uint32_t version = R.u16();
   if (!R.ok || version != 1) return bad("version: expected 1");
   cbaa_config c;
@@ -1294,6 +1296,27 @@ int parse_sketch(const void* in, uint64_t n, cbaa_config* out, const uint8_t** p
   if (len != want)
     return bad("payload length field " + std::to_string(len) + " != cube size " + std::to_string(want));
   uint64_t have = (uint64_t)(R.end - R.p);
+  if (sp) {   // u32 block bits, u64 blocks, (blocks + 1) × u64 offsets, streams
+    const uint64_t nb = (len * 8 + 32767) / 32768;
+    if (have < 12 || R.u32() != 32768u) return bad("sparse block bits: expected 32768");
+    if (R.u64() != nb) return bad("sparse block count: expected " + std::to_string(nb));
+    const uint64_t need = 8 * (nb + 1);
+    if ((uint64_t)(R.end - R.p) < need) return bad("sparse offsets truncated");
+    const uint8_t* offs = R.p;
+    uint64_t prev = 0, last = 0;
+    for (uint64_t b = 0; b <= nb; ++b) {   // offsets must start at 0 and never decrease
+      uint64_t v = 0;
+      for (int k = 0; k < 8; ++k) v |= (uint64_t)offs[8 * b + k] << (8 * k);
+      if ((b == 0 && v != 0) || v < prev) return bad("sparse offsets not ascending from 0");
+      prev = last = v;
+    }
+    if ((uint64_t)(R.end - R.p) - need < last)
+      return bad("payload truncated: expected " + std::to_string(last) + " stream bytes");
+    *out = c;
+    if (payload) *payload = R.p;   // offsets, then the streams
+    if (plen) *plen = need + last;
+    return CBAA_OK;
+  }
   if (have < len)
     return bad("payload truncated: expected " + std::to_string(len) + " bytes, got " + std::to_string(have));
   *out = c;
@@ -1303,15 +1326,9 @@ int parse_sketch(const void* in, uint64_t n, cbaa_config* out, const uint8_t** p
 }
 }  // namespace
 
-int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream) {
-  if (!h || !n_written) return CBAA_E_ARG;
-  const cbaa_config& c = h->cfg;
-  const uint64_t hb = sketch_header_bytes(c), total = hb + h->cube_bytes;
-  *n_written = total;
-  if (cap < total || !out) return fail(h, CBAA_E_CAPACITY, "cbaa_serialize: buffer smaller than cbaa_sketch_bytes");
-  DeviceGuard dg(h->device);
-  Writer W{(uint8_t*)out};
-  W.u8('C'); W.u8('B'); W.u8('A'); W.u8('1');
+static void write_sketch_header(const cbaa_config& c, uint64_t cube_bytes, uint8_t* out, char kind) {
+  Writer W{out};
+  W.u8('C'); W.u8('B'); W.u8('A'); W.u8((uint8_t)kind);
   W.u16(1);
   W.u8(c.r); W.u8(c.num_ra); W.u8(c.num_va);
   W.u32(c.g);
@@ -1319,7 +1336,69 @@ int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written,
   for (uint32_t i = 0; i < c.num_ra; ++i) W.u8(c.clbs[i]);
   W.u32(c.mangle_a); W.u32(c.mangle_b); W.u32(c.bv_seed);
   for (uint32_t j = 0; j < c.num_va; ++j) W.u32(c.va_seeds[j]);
-  W.u64(h->cube_bytes);
+  W.u64(cube_bytes);
+}
+
+int cbaa_serialize_sparse(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream) {
+  if (!h || !n_written) return CBAA_E_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t nwords = h->cube_words, nb = (nwords + kSparseBlockWords - 1) / kSparseBlockWords;
+  const uint64_t hb = sketch_header_bytes(h->cfg) + 12 + 8 * (nb + 1);
+  void* scratch = nullptr;   // u32 bytes[nb] | u64 off[nb + 1]
+  CK(h, cudaMalloc(&scratch, nb * 4 + 8 * (nb + 1) + 16));
+  uint32_t* bytes = (uint32_t*)scratch;
+  unsigned long long* off = (unsigned long long*)((char*)scratch + ((nb * 4 + 15) & ~15ull));
+  const int grid = (int)std::min<uint64_t>((uint64_t)h->sms * 16, (nb + 3) / 4);
+  k_sparse_size<<<grid, 128, 0, s>>>(h->cube, nwords, nb, bytes);
+  int rc = launch_check(h, "k_sparse_size");
+  if (!rc) {
+    k_sparse_offsets<<<1, 1024, 0, s>>>(bytes, nb, off);
+    rc = launch_check(h, "k_sparse_offsets");
+  }
+  unsigned long long total = 0;
+  cudaError_t e = cudaSuccess;
+  if (!rc) {
+    e = cudaMemcpyAsync(&total, off + nb, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "sparse size");
+  }
+  *n_written = hb + total;
+  if (!rc && (cap < hb + total || !out))
+    rc = fail(h, CBAA_E_CAPACITY, "cbaa_serialize_sparse: buffer smaller than *n_written");
+  void* dpay = nullptr;
+  if (!rc && total) {
+    e = cudaMalloc(&dpay, total);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMalloc(sparse payload)");
+    if (!rc) {
+      k_sparse_write<<<grid, 128, 0, s>>>(h->cube, nwords, nb, off, (uint8_t*)dpay);
+      rc = launch_check(h, "k_sparse_write");
+    }
+  }
+  if (!rc) {
+    uint8_t* o = (uint8_t*)out;
+    write_sketch_header(h->cfg, h->cube_bytes, o, '2');
+    Writer W{o + sketch_header_bytes(h->cfg)};
+    W.u32(32768);
+    W.u64(nb);
+    e = cudaMemcpyAsync(W.p, off, 8 * (nb + 1), cudaMemcpyDeviceToHost, s);   // little-endian host
+    if (e == cudaSuccess && total) e = cudaMemcpyAsync(o + hb, dpay, total, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "sparse copy-out");
+  }
+  if (dpay) cudaFree(dpay);
+  cudaFree(scratch);
+  return rc;
+}
+
+int cbaa_serialize(cbaa_handle* h, void* out, uint64_t cap, uint64_t* n_written, cbaa_stream stream) {
+  if (!h || !n_written) return CBAA_E_ARG;
+  const cbaa_config& c = h->cfg;
+  const uint64_t hb = sketch_header_bytes(c), total = hb + h->cube_bytes;
+  *n_written = total;
+  if (cap < total || !out) return fail(h, CBAA_E_CAPACITY, "cbaa_serialize: buffer smaller than cbaa_sketch_bytes");
+  DeviceGuard dg(h->device);
+  write_sketch_header(c, h->cube_bytes, (uint8_t*)out, '1');
   cudaStream_t s = (cudaStream_t)stream;
   CK(h, cudaMemcpyAsync((uint8_t*)out + hb, h->cube, h->cube_bytes, cudaMemcpyDeviceToHost, s));
   CK(h, cudaStreamSynchronize(s));
@@ -1341,7 +1420,8 @@ int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_
   const uint8_t* payload = nullptr;
   uint64_t plen = 0;
   std::string why;
-  if (parse_sketch(in, n, &fc, &payload, &plen, &why)) return fail(h, CBAA_E_CONFIG, "SketchFile: " + why);
+  bool sparse = false;
+  if (parse_sketch(in, n, &fc, &payload, &plen, &why, &sparse)) return fail(h, CBAA_E_CONFIG, "SketchFile: " + why);
   const cbaa_config& c = h->cfg;
   auto mismatch = [&](const char* field) {
     return fail(h, CBAA_E_MISMATCH, std::string("SketchFile refused: field '") + field + "' differs from this cube");
@@ -1361,6 +1441,32 @@ int cbaa_deserialize(cbaa_handle* h, const void* in, uint64_t n, int mode, cbaa_
     if (fc.va_seeds[j] != c.va_seeds[j]) return mismatch("va_seeds");
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (sparse) {   // offsets + streams to the device, then one thread per block ORs its bits in
+    const uint64_t nb = (h->cube_words + kSparseBlockWords - 1) / kSparseBlockWords;
+    void* d = nullptr;   // u32 bad flag | offsets | streams
+    CK(h, cudaMalloc(&d, 16 + plen));
+    int rc = CBAA_OK;
+    cudaError_t e = cudaMemsetAsync(d, 0, 16, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)d + 16, payload, plen, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && mode == CBAA_SKETCH_REPLACE) e = cudaMemsetAsync(h->cube, 0, h->cube_bytes, s);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "sparse SketchFile copy-in");
+    if (!rc) {
+      const unsigned long long* off = (const unsigned long long*)((char*)d + 16);
+      const int grid = (int)std::min<uint64_t>((uint64_t)h->sms * 8, (nb + 127) / 128);
+      k_sparse_decode<<<grid, 128, 0, s>>>((const uint8_t*)(off + nb + 1), off, nb, h->cube_words, h->cube,
+                                           (uint32_t*)d);
+      rc = launch_check(h, "k_sparse_decode");
+    }
+    uint32_t bad = 0;
+    if (!rc) {
+      e = cudaMemcpyAsync(&bad, d, 4, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(h, e, "sparse SketchFile decode");
+    }
+    cudaFree(d);
+    if (!rc && bad) rc = fail(h, CBAA_E_CONFIG, "SketchFile: malformed sparse stream (varint or position out of range)");
+    return rc;
+  }
   if (mode == CBAA_SKETCH_REPLACE) {
     CK(h, cudaMemcpyAsync(h->cube, payload, plen, cudaMemcpyHostToDevice, s));
     CK(h, cudaStreamSynchronize(s));

@@ -1043,3 +1043,159 @@ __global__ void k_or_multicast(uint64_t* __restrict__ dst, const uint64_t* __res
   for (; i < n8; i += stride) dst[i] = mc_or(mc + i);
 }
 }  // namespace cbaa
+
+namespace cbaa {
+// ---------------------------------------------------------------- sparse SketchFile "CBA2"
+// Blocks of 2^15 cube bits = 1024 words; one warp per block, lane l owns words [32l, 32l + 32).  A block's
+// stream is the LEB128 gaps between its ascending set-bit positions.  The first gap of a lane's segment
+// depends on the last set bit of the lanes before it: a warp max-scan of "last set position".
+constexpr uint32_t kSparseBlockWords = 1024;
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t leb128_len(uint32_t v) { return 1u + (v >= 128u) + (v >= (1u << 14)) + (v >= (1u << 21)) + (v >= (1u << 28)); }
+
+// Per lane: first/last set position in its segment (−1 if none) and the bytes of the gaps inside it.
+struct SparseSeg {
+  int32_t first, last;
+  uint32_t inner_bytes;
+};
+__device__ __forceinline__ SparseSeg sparse_seg(const uint32_t* __restrict__ blk, uint32_t nwords, uint32_t lane) {
+  SparseSeg s{-1, -1, 0};
+  for (uint32_t j = 0; j < 32; ++j) {
+    const uint32_t wi = lane * 32 + j;
+    uint32_t w = wi < nwords ? blk[wi] : 0u;
+    while (w) {
+      const int32_t pos = (int32_t)(wi * 32 + (__ffs(w) - 1));
+      w &= w - 1;
+      if (s.last >= 0) s.inner_bytes += leb128_len((uint32_t)(pos - s.last - 1));
+      else s.first = pos;
+      s.last = pos;
+    }
+  }
+  return s;
+}
+// Last set position of the lanes before this one (−1 if none): exclusive max-scan over the warp.
+__device__ __forceinline__ int32_t prev_last(int32_t last, uint32_t lane) {
+  int32_t v = last;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if ((int)lane >= o) v = max(v, y);
+  }
+  const int32_t ex = __shfl_up_sync(0xffffffffu, v, 1);
+  return lane == 0 ? -1 : ex;
+}
+
+// Pass 1: bytes of each block's stream.
+__global__ void k_sparse_size(const uint32_t* __restrict__ cube, uint64_t nwords, uint64_t nblocks,
+                              uint32_t* __restrict__ bytes) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nblocks; b += nw) {
+    const uint64_t w0 = b * kSparseBlockWords;
+    const uint32_t n = (uint32_t)umin64(kSparseBlockWords, nwords - w0);
+    const SparseSeg s = sparse_seg(cube + w0, n, lane);
+    const int32_t pl = prev_last(s.last, lane);
+    uint32_t my = s.inner_bytes + (s.first >= 0 ? leb128_len((uint32_t)(s.first - pl - 1)) : 0u);
+    my = warp_sum(my);
+    if (lane == 0) bytes[b] = my;
+  }
+}
+
+// Exclusive prefix of the block sizes (one CTA of 1024 threads): off[b], off[nblocks] = total.
+__global__ void __launch_bounds__(1024) k_sparse_offsets(const uint32_t* __restrict__ bytes, uint64_t nblocks,
+                                                         unsigned long long* __restrict__ off) {
+  __shared__ unsigned long long s_w[32];
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint64_t per = (nblocks + 1023) / 1024, b0 = umin64(t * per, nblocks), b1 = umin64(b0 + per, nblocks);
+  unsigned long long loc = 0;
+  for (uint64_t b = b0; b < b1; ++b) loc += bytes[b];
+  unsigned long long incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  unsigned long long run = incl - loc, tot = 0;
+  for (int w = 0; w < 32; ++w) {
+    run += w < (int)warp ? s_w[w] : 0ull;
+    tot += s_w[w];
+  }
+  for (uint64_t b = b0; b < b1; ++b) {
+    off[b] = run;
+    run += bytes[b];
+  }
+  if (t == 0) off[nblocks] = tot;
+}
+
+// Pass 2: the streams, at off[b] + (bytes of the lanes before) in out.
+__global__ void k_sparse_write(const uint32_t* __restrict__ cube, uint64_t nwords, uint64_t nblocks,
+                               const unsigned long long* __restrict__ off, uint8_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nblocks; b += nw) {
+    const uint64_t w0 = b * kSparseBlockWords;
+    const uint32_t n = (uint32_t)umin64(kSparseBlockWords, nwords - w0);
+    const uint32_t* blk = cube + w0;
+    const SparseSeg s = sparse_seg(blk, n, lane);
+    int32_t prev = prev_last(s.last, lane);
+    const uint32_t my = s.inner_bytes + (s.first >= 0 ? leb128_len((uint32_t)(s.first - prev - 1)) : 0u);
+    uint32_t incl = my;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    uint8_t* p = out + off[b] + (incl - my);
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t wi = lane * 32 + j;
+      uint32_t w = wi < n ? blk[wi] : 0u;
+      while (w) {
+        const int32_t pos = (int32_t)(wi * 32 + (__ffs(w) - 1));
+        w &= w - 1;
+        uint32_t gap = (uint32_t)(pos - prev - 1);
+        while (gap >= 128u) {
+          *p++ = (uint8_t)(0x80u | (gap & 0x7Fu));
+          gap >>= 7;
+        }
+        *p++ = (uint8_t)gap;
+        prev = pos;
+      }
+    }
+  }
+}
+
+// Decode (one thread per block): OR the block's set bits into the cube; a malformed stream (a varint
+// past its end, a position past the block) sets *bad.
+__global__ void k_sparse_decode(const uint8_t* __restrict__ in, const unsigned long long* __restrict__ off,
+                                uint64_t nblocks, uint64_t nwords, uint32_t* __restrict__ cube, uint32_t* bad) {
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = off[b + 1], w0 = b * kSparseBlockWords;
+    const uint64_t nbits = umin64(kSparseBlockWords, nwords - w0) * 32;
+    uint64_t k = off[b];
+    int64_t prev = -1;
+    while (k < e) {
+      uint64_t gap = 0;
+      int shift = 0;
+      bool okv = false;
+      while (k < e && shift <= 28) {
+        const uint8_t byte = in[k++];
+        gap |= (uint64_t)(byte & 0x7Fu) << shift;
+        shift += 7;
+        if (!(byte & 0x80u)) {
+          okv = true;
+          break;
+        }
+      }
+      const int64_t pos = prev + 1 + (int64_t)gap;
+      if (!okv || pos >= (int64_t)nbits) {
+        atomicExch(bad, 1u);
+        break;
+      }
+      atomicOr(cube + w0 + (pos >> 5), 1u << (pos & 31));
+      prev = pos;
+    }
+  }
+}
+}  // namespace cbaa

@@ -156,3 +156,56 @@ def test_sparse_roundtrip_and_size(paper, density):
         want += int(np.sum(1 + (gaps >= 128) + (gaps >= 1 << 14) + (gaps >= 1 << 21)))
     nb = -(-n * 8 // 32768)
     assert len(data) == hb + 12 + 8 * (nb + 1) + want
+
+
+def test_sparse_header_parsed_by_library(paper):
+    """cbaa_sketch_config reads the oracle's CBA2 header; broken offsets or streams are refused by name."""
+    p = dict(paper, **ODD)
+    n = O.cube_bytes(p)
+    cube = np.packbits(np.random.default_rng(3).random(n * 8) < 0.01, bitorder="little")
+    data = O.serialize_sparse(p, cube)
+    d = cb.sketch_config(data).to_dict()
+    for k in ("r", "num_ra", "num_va", "g", "cbn", "clbs", "mangle_a", "mangle_b", "bv_seed", "va_seeds"):
+        assert d[k] == p[k], k
+    hb = len(O.serialize(p, cube[:0]))
+    for mutate, field in [(lambda b: b[:hb] + b"\x00\x40\x00\x00" + b[hb + 4:], "block bits"),
+                          (lambda b: b[:hb + 12] + b"\x01" + b[hb + 13:], "offsets"),
+                          (lambda b: b[:-3], "truncated")]:
+        with pytest.raises(cb.CbaaError) as e:
+            cb.sketch_config(mutate(data))
+        assert field in str(e.value), (field, str(e.value))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["paper", "odd"])
+def test_device_sparse_file_matches_oracle(paper, name):
+    """cbaa_serialize_sparse on the device == the oracle's CBA2 bytes; REPLACE and MERGE of the file
+    reproduce the cube; a corrupted stream is refused."""
+    torch = pytest.importorskip("torch")
+    p = paper if name == "paper" else dict(paper, **ODD)
+    w = W.generate(W.C1, 12)
+    h = cb.Cbaa(cb.config_from_dict(p), 0)
+    h.reset()
+    h.update(torch.from_numpy(w.src.view(np.int32)).cuda(), torch.from_numpy(w.dst.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    ref, _ = O.update(p, w.src, w.dst)
+    data = h.serialize_sparse()
+    want = O.serialize_sparse(p, ref)
+    assert data.tobytes() == want
+    assert len(want) < O.cube_bytes(p)            # C1 at these geometries: sparse is smaller
+    g = cb.Cbaa(cb.config_from_dict(p), 0)
+    g.reset()
+    g.deserialize(data)
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cube().cpu().numpy(), ref)
+    g.deserialize(O.serialize(p, ref), merge=True)   # MERGE of the same bits: unchanged
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cube().cpu().numpy(), ref)
+    h.reset()
+    h.deserialize(data, merge=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(h.cube().cpu().numpy(), ref)
+    bad = bytearray(want)
+    bad[-1] = 0x80                                 # last varint left unterminated
+    with pytest.raises(cb.CbaaError):
+        g.deserialize(bytes(bad))
