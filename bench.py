@@ -610,6 +610,7 @@ def main():
                            "words, 64 MiB L2-resident) measured in this run; > 1 means the design sets more "
                            "bits per second than one L2 RED each could (binned: ORs done in shared memory)"},
         # ncu bytes/REDs come from one 100M-pair C2 update: scaled per pair to this run's update
+        "l2_hit_pct": {k: (nb.get(k) or {}).get("l2_hit_pct") for k in nb if k.startswith("k_bin")},
         "dram": {"bytes_per_update": ncu_per_pair("dram_bytes") * n if ncu_per_pair("dram_bytes") else None,
                  "algorithmic_bytes": algo_in,
                  "ratio": ncu_per_pair("dram_bytes") / 8 if ncu_per_pair("dram_bytes") else None,

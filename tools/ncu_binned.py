@@ -10,7 +10,7 @@ from ncu_summary import main as _summary  # noqa: E402
 
 FIELDS = ("dram_read_bytes", "dram_write_bytes", "duration_us", "red_requests_to_l2", "red_sectors_to_l2",
           "atom_requests_to_l2", "smem_wavefronts", "smem_bank_conflicts", "warps_active_pct",
-          "l1tex_throughput_pct", "registers")
+          "l1tex_throughput_pct", "registers", "l2_hit_pct", "lts_throughput_avg_pct", "dram_throughput_pct")
 
 
 def main(path, how=""):
