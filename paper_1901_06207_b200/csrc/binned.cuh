@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
                                                              uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e,
                                                              unsigned long long* __restrict__ skipped) {
   constexpr uint32_t nbins = kWBins;
+  static_assert(nbins % kBinThreads == 0 && kBinTile <= 0xffff, "bins per thread whole, rank fits 16 bits");
   constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread
   constexpr uint32_t wchunk = kPerLane * 32;              // 128 bins per warp
   extern __shared__ __align__(16) uint64_t smw[];
