@@ -869,11 +869,12 @@ __global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_w(const __grid_
     p = pn;
   }
   __syncthreads();
-  // image word h·16384 + i = word (2·wq + h) of column i of CS cs
+  // image word h·16384 + i = word (2·wq + h) of column i of CS cs: the two halves of a column
+  // are adjacent cube words, OR-ed in with one 64-bit RED (half the L2 atomics of two 32-bit ones)
   uint32_t* cw = cube + (uint64_t)cs * G.cs_words + 2u * wq;
-  for (uint32_t i = threadIdx.x; i < 2 * kCols; i += kWApplyThreads) {
-    const uint32_t v = sub[i];
-    if (v) red_or(cw + (uint64_t)(i & (kCols - 1u)) * G.wpc + (i >> 14), v);
+  for (uint32_t i = threadIdx.x; i < kCols; i += kWApplyThreads) {
+    const uint32_t v0 = sub[i], v1 = sub[kCols + i];
+    if (v0 | v1) red_or64(reinterpret_cast<unsigned long long*>(cw + (uint64_t)i * G.wpc), ((uint64_t)v1 << 32) | v0);
   }
 }
 

@@ -30,6 +30,10 @@ __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_or64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_stream4(const uint32_t* p) {
   // input pairs are read exactly once: evict-first so they do not displace the cube in L2
   return __ldcs(reinterpret_cast<const uint4*>(p));
