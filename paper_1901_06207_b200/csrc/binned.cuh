@@ -584,12 +584,6 @@ __device__ __forceinline__ uint32_t lds(uint32_t a) {
 __device__ __forceinline__ void reds_or(uint32_t a, uint32_t bit) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit));
 }
-// RED.OR of `bit` unless the loaded word v already has it, as one predicated instruction (a C++ `if`
-// around the asm costs a BSSY/BRA/BSYNC triple per array and entry)
-__device__ __forceinline__ void reds_or_if_clear(uint32_t a, uint32_t bit, uint32_t v) {
-  asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %2, 0;\n @p red.shared.or.b32 [%0], %1;\n}" ::"r"(a), "r"(bit),
-               "r"(v & bit));
-}
 
 // ---------------------------------------------------------------- wide entries (the paper configuration)
 // With r = 4 a 32-bit entry holds LP (28 bits) and only s = 4 row bits, so a word group (32 rows) is
@@ -842,8 +836,12 @@ __global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_w(const __grid_
       adr[a] = hb + 16384u * (uint32_t)a + 4u * c[a];
       v[a] = lds(adr[a]);
     }
+    // one branch per entry (a predicated shared atomic compiles to a branch each): most entries repeat
+    // an earlier one and find all four bits set; the rest OR each word with its missing bit (or 0)
+    if (!(v[0] & v[1] & v[2] & v[3] & bit)) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) reds_or_if_clear(adr[a], bit, v[a]);
+      for (int a = 0; a < 4; ++a) reds_or(adr[a], bit & ~v[a]);
+    }
   };
   constexpr uint32_t kStep = kApplyUnroll * kWApplyThreads;
   uint64_t e[kApplyUnroll];
@@ -957,8 +955,13 @@ __global__ void __launch_bounds__(kApplyThreads, 3) k_bin_apply(const __grid_con
         adr[a] = (P ? sbase + 16384u * (uint32_t)a : ab[a]) + 4u * col;
         v[a] = lds(adr[a]);
       }
+      uint32_t all = bit;   // one branch per entry (see k_bin_apply_w)
 #pragma unroll
-      for (int a = 0; a < NRA + NVA; ++a) reds_or_if_clear(adr[a], bit, v[a]);
+      for (int a = 0; a < NRA + NVA; ++a) all &= v[a];
+      if (!all) {
+#pragma unroll
+        for (int a = 0; a < NRA + NVA; ++a) reds_or(adr[a], bit & ~v[a]);
+      }
     } else {
       for (uint32_t a = 0; a < narr; ++a) {
         const uint32_t adr = sbase + 4u * ((G.arr_off[a] >> G.wpc_log2) + lp_col(G, dbl, lp, a));
