@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
   const uint32_t w0 = warp * wchunk;
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
-    // key = (row mod 64) << 24 | bin << 14 | rank in the tile; ent = LP
+    // key = cs << 28 | row << 16 | rank in the tile (bin = key >> 22); ent = LP
     uint32_t key[kBinPPT], ent[kBinPPT];
     const bool whole = vec && t0 + kBinTile <= c1;
     if (whole) {
