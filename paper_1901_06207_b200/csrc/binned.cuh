@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
                                                              uint32_t* __restrict__ entries,
                                                              const uint32_t* __restrict__ start,
                                                              uint32_t* __restrict__ log_n, uint32_t* __restrict__ log_e,
-                                                             uint16_t* __restrict__ log_b) {
+                                                             uint16_t* __restrict__ log_b, uint32_t pf) {
   extern __shared__ uint32_t sm[];
   uint32_t* base = sm;                                   // [nbins] this tile's reserved slot of each bin
   uint32_t* toff = base + B.nbins;                       // [nbins + 1] tile counts → exclusive offsets
@@ -316,6 +316,11 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter(cons
       }
     }
     __syncthreads();
+    // L2 prefetch of the next tile after the rank barrier (as in k_bin_scatter_w; pf: distance in tiles)
+    if ((pf & 255u) && vec && tid == 0) {
+      const uint64_t tp = t0 + (uint64_t)(pf & 255u) * kBinTile;
+      if (tp + kBinTile <= c1) prefetch_l2(src + tp, kBinTile * 4), prefetch_l2(dst + tp, kBinTile * 4);
+    }
     // Warp w owns bins [w·wchunk, (w+1)·wchunk): in row j (32 consecutive bins) lane l owns bin
     // 32j + ((l + j) mod 32), so a warp touches 32 consecutive words per row (conflict-free, and its 32
     // reservation atomics hit one line of the cursors; 16 in flight per thread).  Then each bin gets its
@@ -617,7 +622,8 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
                                                              uint64_t* __restrict__ entries,
                                                              const uint32_t* __restrict__ start,
                                                              uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e,
-                                                             unsigned long long* __restrict__ skipped) {
+                                                             unsigned long long* __restrict__ skipped,
+                                                             uint32_t pf) {
   constexpr uint32_t nbins = kWBins;
   static_assert(nbins % kBinThreads == 0 && kBinTile <= 0xffff, "bins per thread whole, rank fits 16 bits");
   constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread
@@ -655,8 +661,23 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), toff_sa = pin(smem_addr(toff));
   const uint32_t w0 = warp * wchunk;
+  // L2 prefetch of the CTA's next tile (pf = distance in tiles | issue point << 8; 0: off): one bulk
+  // prefetch per array (32 KiB each) by one thread, so the next tile's loads wait on L2 rather than DRAM.
+  // Issued after the rank barrier (point 1, the default), once this tile's own loads have returned:
+  // issued at the tile start (point 0) it competes with them, issued before the write-out (point 2) it
+  // lands late; distance 2+ is slower (profiles/r02_scatter_ab.md).
+  const uint32_t pfd = vec ? (pf & 255u) : 0u, pfat = pf >> 8;
+  auto prefetch_tile = [&](uint64_t tp) {
+    if (tp + kBinTile <= c1) prefetch_l2(src + tp, kBinTile * 4), prefetch_l2(dst + tp, kBinTile * 4);
+  };
+  if (tid == 0)
+    for (uint32_t j = 1; j < pfd; ++j) prefetch_tile(c0 + (uint64_t)j * kBinTile);
   __syncthreads();
   for (uint64_t t0 = c0; t0 < c1; t0 += kBinTile) {
+    auto prefetch_next = [&](uint32_t at) {
+      if (pfd && pfat == at && tid == 0) prefetch_tile(t0 + (uint64_t)pfd * kBinTile);
+    };
+    prefetch_next(0);
     // key = cs << 28 | row << 16 | rank in the tile (bin = key >> 22); ent = LP
     uint32_t key[kBinPPT], ent[kBinPPT];
     const bool whole = vec && t0 + kBinTile <= c1;
@@ -706,6 +727,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
       }
     }
     __syncthreads();
+    prefetch_next(1);
     // per-bin reservation and offsets (rotated lane ownership as in k_bin_scatter)
     {
       uint32_t x[kPerLane], r[kPerLane], loc = 0;
@@ -763,6 +785,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
         if (key[i] != 0xffffffffu) stage_one(i);
     }
     __syncthreads();
+    prefetch_next(2);
     const uint32_t total = toff[nbins];
     if (!s_ovf && total == kBinTile) {   // a full tile: compile-time trip count, no bounds tests
 #pragma unroll 8

@@ -97,6 +97,7 @@ struct cbaa_handle {
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
   int bin_wide = 0;               // the paper configuration: 64-bit entries, 1024 bins (k_bin_scatter_w, binned.cuh)
   BinGeo BW{};                    // bin geometry of the wide path
+  uint32_t scatter_pf = 1 | 1u << 8;   // k_bin_scatter_w L2 prefetch: distance in tiles | issue point << 8 (CBAA_SCATTER_PF)
   bool apply_paper = false;       // k_bin_apply<3, 1, 4, true>: the paper's default configuration
   uint32_t bin_sample_log2 = 9;   // regions sized from 8 pairs of every 2^L (0: exact count; CBAA_BIN_SAMPLE)
   uint64_t bin_sample_min = 1ull << 24;   // chunks with fewer pairs are counted exactly (CBAA_BIN_SAMPLE_MIN)
@@ -528,10 +529,11 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
       if (prefix)
         k_bin_scatter_w<true><<<B.nblk, kBinThreads, kWScatterSmemPrefix, s>>>(
             h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log,
-            sl ? h->skipped : nullptr);
+            sl ? h->skipped : nullptr, h->scatter_pf);
       else
         k_bin_scatter_w<false><<<B.nblk, kBinThreads, kWScatterSmem, s>>>(
-            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log, nullptr);
+            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log, nullptr,
+            h->scatter_pf);
     } else if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
       const uint32_t nw = (uint32_t)h->sms;
       const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
@@ -542,16 +544,16 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     } else {           // tile counting sort (default)
       if (prefix)
         k_bin_scatter<true, 0><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
-                                                                  start, log_n, log_e, log_b);
+                                                                  start, log_n, log_e, log_b, h->scatter_pf);
       else if (B.nbins == 4096 && h->G.r == 4 && h->G.g == 4096)   // the paper geometry: constants inlined
         k_bin_scatter<false, -1><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
-                                                                    start, log_n, log_e, log_b);
+                                                                    start, log_n, log_e, log_b, h->scatter_pf);
       else if (B.nbins == 4096)   // bin loops with compile-time trip counts
         k_bin_scatter<false, 4096><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
-                                                                      start, log_n, log_e, log_b);
+                                                                      start, log_n, log_e, log_b, h->scatter_pf);
       else
         k_bin_scatter<false, 0><<<B.nblk, kBinThreads, sm_sc, s>>>(h->G, B, a, b, m, per, vec, cursor, h->bin_ent,
-                                                                   start, log_n, log_e, log_b);
+                                                                   start, log_n, log_e, log_b, h->scatter_pf);
     }
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
@@ -739,6 +741,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
                  : bm                 ? std::strtoull(bm, nullptr, 10)
                                       : std::max<uint64_t>(1u << 20, h->cube_words / 4);
+    if (const char* e = std::getenv("CBAA_SCATTER_PF")) h->scatter_pf = (uint32_t)std::strtoul(e, nullptr, 10);
     const char* bc = std::getenv("CBAA_BIN_CHUNK");
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));

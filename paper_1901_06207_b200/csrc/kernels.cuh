@@ -39,6 +39,11 @@ __device__ __forceinline__ uint4 ld_stream4(const uint32_t* p) {
   return __ldcs(reinterpret_cast<const uint4*>(p));
 }
 
+// one bulk prefetch of [p, p + bytes) into L2 (16-B aligned address and size; no registers, no shared memory)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
