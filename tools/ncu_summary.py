@@ -24,6 +24,8 @@ KEYS = {
     "global_load_sectors": ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 1.0),
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
+    "ipc_per_sm": ("sm__inst_executed.avg.per_cycle_active", 1.0),
+    "warp_instructions": ("smsp__inst_executed.sum", 1.0),
     "registers": ("launch__registers_per_thread", 1.0),
     "grid": ("launch__grid_size", 1.0),
     "block": ("launch__block_size", 1.0),
@@ -49,6 +51,13 @@ def main(path):
             if k == "duration_us":
                 v *= UNIT.get(u, 1)
             e[k] = v
+        # stall reasons: warps stalled per issued instruction, by reason (largest first)
+        st = {}
+        for m, v in d.items():
+            if m.startswith("smsp__average_warps_issue_stalled_") and m.endswith("_per_issue_active.ratio") and v not in ("", "n/a"):
+                st[m[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(v.replace(",", ""))
+        if st:
+            e["stalls_per_issue"] = dict(sorted(((k, round(x, 3)) for k, x in st.items() if x >= 0.01), key=lambda kv: -kv[1]))
         res.append(e)
     json.dump({"source": path, "launches": res}, sys.stdout, indent=1)
 
