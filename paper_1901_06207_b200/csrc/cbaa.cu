@@ -97,6 +97,7 @@ struct cbaa_handle {
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
   int bin_wide = 0;               // the paper configuration: 64-bit entries, 1024 bins (k_bin_scatter_w, binned.cuh)
   BinGeo BW{};                    // bin geometry of the wide path
+  uint32_t sample_ctas = 0;       // k_bin_sample grid (0: one CTA per SM; CBAA_SAMPLE_CTAS)
   uint32_t scatter_pf = 1 | 1u << 8;   // k_bin_scatter_w L2 prefetch: distance in tiles | issue point << 8 (CBAA_SCATTER_PF)
   bool apply_paper = false;       // k_bin_apply<3, 1, 4, true>: the paper's default configuration
   uint32_t bin_sample_log2 = 9;   // regions sized from 8 pairs of every 2^L (0: exact count; CBAA_BIN_SAMPLE)
@@ -509,10 +510,11 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     const uint64_t per_c = (((m + nc - 1) / nc) + 3) & ~3ull;
     const uint32_t sl = samp && m >= h->bin_sample_min ? samp : 0u;
     int tk = t_begin(h, 0, s);
+    const uint32_t ns = h->sample_ctas ? h->sample_ctas : (uint32_t)h->sms;   // 1.5 µs faster than 2 per SM
     if (sl && prefix)
-      k_bin_sample<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
+      k_bin_sample<true><<<ns, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
     else if (sl)
-      k_bin_sample<false><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
+      k_bin_sample<false><<<ns, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, sl, vec, counts);
     else if (prefix)
       k_bin_count<true><<<nc, kCountThreads, sm_cnt, s>>>(h->G, B, a, b, m, per_c, vec, counts, h->skipped);
     else
@@ -741,6 +743,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
                  : bm                 ? std::strtoull(bm, nullptr, 10)
                                       : std::max<uint64_t>(1u << 20, h->cube_words / 4);
+    if (const char* e = std::getenv("CBAA_SAMPLE_CTAS")) h->sample_ctas = (uint32_t)std::strtoul(e, nullptr, 10);
     if (const char* e = std::getenv("CBAA_SCATTER_PF")) h->scatter_pf = (uint32_t)std::strtoul(e, nullptr, 10);
     const char* bc = std::getenv("CBAA_BIN_CHUNK");
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
