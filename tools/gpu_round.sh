@@ -6,7 +6,8 @@
 #   bench     bench.py N=1 (C2, default); bench_c3 / bench_c4: the other workloads; ref: --impl reference
 #   launches  ncu launch list (gpu__time_duration, clock-control none) of a short bench run
 #   ncu       ncu --set full of one binned update + one detect → ncu_binned_TAG.json
-#   sanitize  compute-sanitizer memcheck/racecheck/synccheck/initcheck of tools/sanitize.py
+#   sanitize  compute-sanitizer memcheck/racecheck/synccheck/initcheck of tools/sanitize.py (closed on the
+#             GPU pool since run r02j: the tool refuses to run there)
 #   sweep     tests/sweep_c5.py (C5 accuracy/throughput sweep)
 #   c4full    tests/full_c4.py (config 4 at full size)
 #   func2     functional N = 2 runs on ONE GPU (gloo process group, IPC exchange with device barriers):
