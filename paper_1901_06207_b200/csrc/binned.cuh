@@ -49,8 +49,8 @@ constexpr int kCountThreads = 1024;
 #ifndef CBAA_CUR_STRIDE
 #define CBAA_CUR_STRIDE 1
 #endif
-// bin b's write cursor is cursor[b · kCurStride]: one 128-B line per cursor, so the scatter's
-// reservation atomics on different bins never queue behind each other in one L2 line
+// bin b's write cursor is cursor[b · kCurStride]; adjacent cursors (stride 1) measured fastest — a warp's
+// 32 reservation atomics then go to one L2 line (strides 8 / 32: profiles/r02_scatter_ab.md)
 constexpr uint32_t kCurStride = CBAA_CUR_STRIDE;
 
 template <bool PREFIX>
