@@ -612,14 +612,23 @@ constexpr int kWBins = 1024;                   // 2^4 CSs × 4096 / 64 rows
 #endif
 constexpr int kWApplyThreads = CBAA_WAPPLY_THREADS;
 constexpr uint64_t kWEntMask = (1ull << 48) - 1;   // staged entry: bin << 48 | LP << 6 | row mod 64
-constexpr size_t kWScatterSmem = (size_t)kBinTile * 8 + (3 * kWBins + 1) * 4;   // 76 KiB: two CTAs per SM
-constexpr size_t kWScatterSmemPrefix = kWScatterSmem + 4096 * 4;                // + the a0 class table
+__host__ __device__ constexpr uint32_t ilog2c(uint32_t v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+// stage + base/toff/rend tables (+ the a0 class table): 76 KiB at 1024 bins, two CTAs per SM
+constexpr size_t wscatter_smem(uint32_t nbins, bool prefix) {
+  return (size_t)kBinTile * 8 + (3 * nbins + 1) * 4 + (prefix ? 4096 * 4 : 0);
+}
+constexpr size_t kWScatterSmem = wscatter_smem(kWBins, false);
+constexpr size_t kWScatterSmemPrefix = wscatter_smem(kWBins, true);
 constexpr size_t kWApplySmem = 2 * 16384 * 4;                                   // two word groups, 128 KiB
 
 // PREFIX: raw on-wire pairs, classified by the inner prefixes (a0) with the two 8 KiB bitmaps
 // staged in shared memory; pairs with zero or two inner endpoints are skipped and counted here (every
 // pair passes through this kernel, so the bin regions can still come from a sample).
-template <bool PREFIX>
+// NB < 0: the paper geometry (r = 4, g = 4096: 1024 bins, shifts and masks as immediates); NB = 256..2048:
+// any geometry with g ≥ 64 whose 2^r·g/64 bins number NB (run-time r and g).  Rank key of a pair:
+// bin << (32 − log2 NB) | row mod 64 << (26 − log2 NB) | rank in the tile (the paper's cs << 28 | row << 16
+// | rank when NB = 1024).
+template <bool PREFIX, int NB>
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(const __grid_constant__ Geo G,
                                                              const uint32_t* __restrict__ src,
                                                              const uint32_t* __restrict__ dst, uint64_t n, uint64_t per,
@@ -629,9 +638,12 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
                                                              uint32_t* __restrict__ log_n, uint64_t* __restrict__ log_e,
                                                              unsigned long long* __restrict__ skipped,
                                                              uint32_t pf) {
-  constexpr uint32_t nbins = kWBins;
-  static_assert(nbins % kBinThreads == 0 && kBinTile <= 0xffff, "bins per thread whole, rank fits 16 bits");
-  constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread
+  constexpr bool kPaperW = NB < 0;
+  constexpr uint32_t nbins = kPaperW ? (uint32_t)kWBins : (uint32_t)NB;
+  constexpr uint32_t kBB = ilog2c(nbins), kKeySh = 32 - kBB, kRB = 26 - kBB;   // bin bits, key shift, rank bits
+  static_assert(nbins % kBinThreads == 0 && (1u << kBB) == nbins && kBinTile < (1u << kRB),
+                "bins per thread whole, a power of two, rank field wide enough");
+  constexpr uint32_t kPerLane = nbins / kBinThreads;      // 4 bins per thread at the paper geometry
   constexpr uint32_t wchunk = kPerLane * 32;              // 128 bins per warp
   extern __shared__ __align__(16) uint64_t smw[];
   uint64_t* stage = smw;                                  // [kBinTile] bin << 48 | entry, sorted by bin
@@ -666,6 +678,12 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
   const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = min(n, c0 + per);
   const uint32_t pa = pin(G.mangle_a), pb = pin(G.mangle_b), pbv = pin(G.bv_seed), toff_sa = pin(smem_addr(toff));
   const uint32_t w0 = warp * wchunk;
+  const uint32_t gm = kPaperW ? 4095u : pin(G.g - 1u), rm = kPaperW ? 15u : pin(G.rmask);
+  const uint32_t rr = kPaperW ? 4u : pin(G.r), bpl = kPaperW ? 6u : pin(G.wpc_log2 - 1u);   // log2(g / 64)
+  auto rank_key = [&](uint32_t mi, uint32_t row) {   // bin, row mod 64 and an empty rank field
+    if (kPaperW) return (mi << 28) | (row << 16);                                   // r = 4: cs = mi mod 16
+    return ((((mi & rm) << bpl) | (row >> 6)) << kKeySh) | ((row & 63u) << kRB);
+  };
   // L2 prefetch of the CTA's next tile (pf = distance in tiles | issue point << 8; 0: off): one bulk
   // prefetch per array (32 KiB each) by one thread, so the next tile's loads wait on L2 rather than DRAM.
   // Issued after the rank barrier (point 1, the default), once this tile's own loads have returned:
@@ -710,10 +728,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
 #pragma unroll
       for (int i = 0; i < kBinPPT; ++i) {
         const uint32_t mi = pa * key[i] + pb, mo = pa * ent[i] + pb;         // P:175, Q2
-        const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
-        const uint32_t hi = (mi << 28) | (row << 16);                       // r = 4: cs = mi mod 16
-        ent[i] = mi >> 4;                                                   // LP
-        key[i] = hi | atoms_inc(toff_sa + 4u * (hi >> 22));                 // bin (cs, row >> 6)
+        const uint32_t row = mix32(mo ^ pbv) & gm;
+        const uint32_t hi = rank_key(mi, row);
+        ent[i] = mi >> rr;                                                  // LP
+        key[i] = hi | atoms_inc(toff_sa + 4u * (hi >> kKeySh));             // bin (cs, row >> 6)
       }
     } else {
 #pragma unroll
@@ -728,10 +746,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
           oip = di ? key[i] : ent[i];
         }
         const uint32_t mi = pa * iip + pb, mo = pa * oip + pb;               // P:175, Q2
-        const uint32_t row = mix32(mo ^ pbv) & 4095u;                       // P:230 (g = 4096)
-        const uint32_t hi = (mi << 28) | (row << 16);                       // r = 4: cs = mi mod 16
-        ent[i] = mi >> 4;                                                   // LP
-        const uint32_t rank = atoms_inc_if(toff_sa + 4u * (hi >> 22), ok ? 1u : 0u);
+        const uint32_t row = mix32(mo ^ pbv) & gm;
+        const uint32_t hi = rank_key(mi, row);
+        ent[i] = mi >> rr;                                                  // LP
+        const uint32_t rank = atoms_inc_if(toff_sa + 4u * (hi >> kKeySh), ok ? 1u : 0u);
         key[i] = ok ? hi | rank : 0xffffffffu;
       }
     }
@@ -781,9 +799,9 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_bin_scatter_w(co
     }
     __syncthreads();
     auto stage_one = [&](int i) {
-      const uint32_t bin = key[i] >> 22;
-      const uint32_t pos = toff[bin] + (key[i] & 0xffffu);
-      stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | ((key[i] >> 16) & 63u);
+      const uint32_t bin = key[i] >> kKeySh;
+      const uint32_t pos = toff[bin] + (key[i] & ((1u << kRB) - 1u));
+      stage[pos] = ((uint64_t)bin << 48) | ((uint64_t)ent[i] << 6) | ((key[i] >> kRB) & 63u);
     };
     if (!PREFIX && whole) {   // every pair of the tile is valid: no per-pair test (no reconvergence)
 #pragma unroll
@@ -909,6 +927,98 @@ __global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_w(const __grid_
   for (uint32_t i = threadIdx.x; i < kCols; i += kWApplyThreads) {
     const uint32_t v0 = sub[i], v1 = sub[kCols + i];
     if (v0 | v1) red_or64(reinterpret_cast<unsigned long long*>(cw + (uint64_t)i * G.wpc), ((uint64_t)v1 << 32) | v0);
+  }
+}
+
+// Column of array a (RA: a CL_bs window of LP; VA: H_j(LP)) and its word-group index:
+// the column's position among the CS's Σc(i) columns in S:116 order.
+__device__ __forceinline__ uint32_t wg_col(const Geo& G, uint64_t dbl, uint32_t lp, uint32_t a) {
+  const uint32_t c = a < G.num_ra ? (uint32_t)(dbl >> G.sh[a]) & G.colmask[a]
+                                  : mix32(lp ^ G.va_seeds[a - G.num_ra]) & G.colmask[a];
+  return (G.arr_off[a] >> G.wpc_log2) + c;
+}
+
+// Apply of the wide entries for other geometries (k_bin_scatter_w<·, NB ≥ 0>): bin b = (cs, row >> 6),
+// image sub[h][ncols] of its two word groups (ncols = Σc(i) ≤ 16384, so ≤ 128 KiB), entries LP << 6 | row
+// mod 64; the walk, test-and-set and 64-bit flush of k_bin_apply_w with run-time column extraction.
+// NRA/NVA > 0: that array split at compile time (run-time shifts, masks and seeds).
+template <int NRA, int NVA>
+__global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_wg(const __grid_constant__ Geo G, uint32_t ncols,
+                                                                   const uint32_t* __restrict__ start,
+                                                                   const uint32_t* __restrict__ end,
+                                                                   const uint64_t* __restrict__ entries,
+                                                                   uint32_t* __restrict__ cube) {
+  extern __shared__ uint32_t sub[];
+  const uint32_t sbase = pin(smem_addr(sub));
+  const uint32_t bpl = G.wpc_log2 - 1u;   // log2(bins per CS) = log2(g / 64)
+  const uint32_t b = blockIdx.x, cs = b >> bpl, wq = b & ((1u << bpl) - 1u);
+  for (uint32_t i = threadIdx.x; i < 2 * ncols / 4; i += kWApplyThreads)
+    reinterpret_cast<uint4*>(sub)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const uint32_t narr = NRA > 0 ? (uint32_t)(NRA + NVA) : G.narr, L = G.L;
+  const uint32_t P0 = start[b], E0 = min(end[b * kCurStride], start[b + 1]);
+  const uint64_t* __restrict__ ent = entries + P0;
+  const uint32_t len = E0 - P0;
+  auto set_bits = [&](uint64_t e) {
+    const uint32_t lp = (uint32_t)(e >> 6), r6 = (uint32_t)e & 63u;
+    const uint32_t bit = 1u << (r6 & 31u), hb = sbase + (r6 >> 5) * (4u * ncols);
+    const uint64_t dbl = ((uint64_t)lp << L) | lp;
+    uint32_t adr[CBAA_MAX_ARRAYS], v[CBAA_MAX_ARRAYS], all = bit;
+#pragma unroll
+    for (uint32_t a = 0; a < CBAA_MAX_ARRAYS; ++a)
+      if (a < narr) {
+        adr[a] = hb + 4u * wg_col(G, dbl, lp, a);
+        v[a] = lds(adr[a]);
+        all &= v[a];
+      }
+    if (!all) {
+#pragma unroll
+      for (uint32_t a = 0; a < CBAA_MAX_ARRAYS; ++a)
+        if (a < narr) reds_or(adr[a], bit & ~v[a]);
+    }
+  };
+  constexpr uint32_t kStep = kApplyUnroll * kWApplyThreads;
+  uint64_t e[kApplyUnroll];
+  uint32_t p = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kWApplyThreads < len ? __ldcs(ent + p + u * kWApplyThreads) : 0ull;
+  while (p < len) {
+    const uint32_t pn = p + kStep;
+    uint64_t en[kApplyUnroll];
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      en[u] = pn + u * kWApplyThreads < len ? __ldcs(ent + pn + u * kWApplyThreads) : 0ull;
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      if (p + u * kWApplyThreads < len) set_bits(e[u]);
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
+    p = pn;
+  }
+  __syncthreads();
+  uint32_t* cw = cube + (uint64_t)cs * G.cs_words + 2u * wq;
+  for (uint32_t i = threadIdx.x; i < ncols; i += kWApplyThreads) {
+    const uint32_t v0 = sub[i], v1 = sub[ncols + i];
+    if (v0 | v1) red_or64(reinterpret_cast<unsigned long long*>(cw + (uint64_t)i * G.wpc), ((uint64_t)v1 << 32) | v0);
+  }
+}
+
+// Overflow log of the generic wide scatter: records bin << 48 | LP << 6 | row mod 64, applied with the
+// direct update's test-and-set.
+__global__ void k_bin_log_wg(const __grid_constant__ Geo G, const uint32_t* __restrict__ log_n,
+                             const uint64_t* __restrict__ log_e, uint32_t* __restrict__ cube) {
+  const uint32_t nrec = *log_n;
+  const uint32_t bpl = G.wpc_log2 - 1u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+    const uint64_t v = log_e[i];
+    const uint32_t bin = (uint32_t)(v >> 48), cs = bin >> bpl;
+    const uint32_t row = ((bin & ((1u << bpl) - 1u)) << 6) | ((uint32_t)v & 63u), bit = 1u << (row & 31u);
+    const uint32_t lp = (uint32_t)((v & kWEntMask) >> 6);
+    const uint64_t dbl = ((uint64_t)lp << G.L) | lp;
+    for (uint32_t a = 0; a < G.narr; ++a) {
+      uint32_t* w = cube + (uint64_t)cs * G.cs_words + (uint64_t)wg_col(G, dbl, lp, a) * G.wpc + (row >> 5);
+      if (!(__ldca(w) & bit)) red_or(w, bit);
+    }
   }
 }
 

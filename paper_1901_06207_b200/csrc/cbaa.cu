@@ -96,6 +96,10 @@ struct cbaa_handle {
   void* bin_log = nullptr;        // k_bin_wc overflow log
   int bin_wc = 0;                 // scatter: tile sort k_bin_scatter (0, default) or write-combining k_bin_wc (1)
   int bin_wide = 0;               // the paper configuration: 64-bit entries, 1024 bins (k_bin_scatter_w, binned.cuh)
+  int bin_wide_gen = 0;           // other geometries with 256-2048 wide bins (k_bin_scatter_w<·, NB>, k_bin_apply_wg)
+  int bin_narrow_ok = 0;          // the 32-bit-entry kernels' tables fit (nbins ≤ 4096, Σc(i) ≤ 28672)
+  int bin_gen_ok = 0;             // the generic wide kernels fit
+  int bin_gen_pref = 0;           // ... and are preferred over the 32-bit-entry kernels
   BinGeo BW{};                    // bin geometry of the wide path
   uint32_t sample_ctas = 0;       // k_bin_sample grid (0: one CTA per SM; CBAA_SAMPLE_CTAS)
   uint32_t scatter_pf = 1 | 1u << 8;   // k_bin_scatter_w L2 prefetch: distance in tiles | issue point << 8 (CBAA_SCATTER_PF)
@@ -452,11 +456,40 @@ void t_end(cbaa_handle* h, int k, cudaStream_t s) {
   if (k >= 0) cudaEventRecord(h->tev[2 * k + 1], s);
 }
 
+// the binned path can run: wide entries (paper or generic geometry), or the 32-bit-entry kernels' tables fit
+bool binned_ok(const cbaa_handle* h) {
+  const bool wide = (h->bin_wide || h->bin_wide_gen) && !h->bin_wc;
+  return h->binnable && (wide || h->bin_narrow_ok);
+}
+
+template <int NB>
+void set_wscatter_attrs() {
+  const uint32_t nb = NB < 0 ? (uint32_t)kWBins : (uint32_t)NB;
+  cudaFuncSetAttribute(k_bin_scatter_w<false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wscatter_smem(nb, false));
+  cudaFuncSetAttribute(k_bin_scatter_w<false, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_bin_scatter_w<true, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wscatter_smem(nb, true));
+  cudaFuncSetAttribute(k_bin_scatter_w<true, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+// Launch of the wide scatter: NB < 0 the paper geometry, else the bin count of a generic wide geometry.
+template <int NB>
+void launch_wscatter(bool prefix, const Geo& G, uint32_t nblk, cudaStream_t s, const uint32_t* a, const uint32_t* b,
+                     uint64_t m, uint64_t per, int vec, uint32_t* cursor, uint64_t* ent, const uint32_t* start,
+                     uint32_t* log_n, uint64_t* lg, unsigned long long* skipped, uint32_t pf) {
+  const uint32_t nb = NB < 0 ? (uint32_t)kWBins : (uint32_t)NB;
+  if (prefix)
+    k_bin_scatter_w<true, NB><<<nblk, kBinThreads, wscatter_smem(nb, true), s>>>(G, a, b, m, per, vec, cursor, ent, start,
+                                                                                 log_n, lg, skipped, pf);
+  else
+    k_bin_scatter_w<false, NB><<<nblk, kBinThreads, wscatter_smem(nb, false), s>>>(G, a, b, m, per, vec, cursor, ent,
+                                                                                   start, log_n, lg, nullptr, pf);
+}
+
 // Binned update (binned.cuh): count → starts → scatter → apply, in chunks of at most 2^28 pairs.
 int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   const uint64_t kChunk = h->bin_chunk;
   const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-  const bool wide = h->bin_wide && !h->bin_wc;   // 64-bit entries, 1024 bins
+  const bool wide = (h->bin_wide || h->bin_wide_gen) && !h->bin_wc;   // 64-bit entries, (cs, row >> 6) bins
   const BinGeo& B = wide ? h->BW : h->B;
   // + per bin: sector alignment and the write-combining scatter's duplicate padding (8 per CTA)
   const uint32_t slack = h->bin_wc ? 8u * (uint32_t)h->sms : 0u;
@@ -528,14 +561,19 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     if ((rc = launch_check(h, "k_bin_starts"))) return rc;
     tk = t_begin(h, 2, s);
     if (wide) {
-      if (prefix)
-        k_bin_scatter_w<true><<<B.nblk, kBinThreads, kWScatterSmemPrefix, s>>>(
-            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log,
-            sl ? h->skipped : nullptr, h->scatter_pf);
+      auto* ent = (uint64_t*)h->bin_ent;
+      auto* lgw = (uint64_t*)h->bin_log;
+      unsigned long long* sk = sl ? h->skipped : nullptr;
+      if (h->bin_wide)
+        launch_wscatter<-1>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
+      else if (B.nbins == 256)
+        launch_wscatter<256>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
+      else if (B.nbins == 512)
+        launch_wscatter<512>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
+      else if (B.nbins == 1024)
+        launch_wscatter<1024>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
       else
-        k_bin_scatter_w<false><<<B.nblk, kBinThreads, kWScatterSmem, s>>>(
-            h->G, a, b, m, per, vec, cursor, (uint64_t*)h->bin_ent, start, log_n, (uint64_t*)h->bin_log, nullptr,
-            h->scatter_pf);
+        launch_wscatter<2048>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
     } else if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
       const uint32_t nw = (uint32_t)h->sms;
       const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
@@ -560,9 +598,15 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     t_end(h, tk, s);
     if ((rc = launch_check(h, h->bin_wc ? "k_bin_wc" : "k_bin_scatter"))) return rc;
     tk = t_begin(h, 3, s);
-    if (wide)
+    if (wide && h->bin_wide)
       k_bin_apply_w<<<B.nbins, kWApplyThreads, kWApplySmem, s>>>(h->G, start, cursor, (const uint64_t*)h->bin_ent,
                                                                  h->cube);
+    else if (wide && h->G.num_ra == 3 && h->G.num_va == 1)
+      k_bin_apply_wg<3, 1><<<B.nbins, kWApplyThreads, (size_t)B.ncols * 8, s>>>(h->G, B.ncols, start, cursor,
+                                                                              (const uint64_t*)h->bin_ent, h->cube);
+    else if (wide)
+      k_bin_apply_wg<0, 0><<<B.nbins, kWApplyThreads, (size_t)B.ncols * 8, s>>>(h->G, B.ncols, start, cursor,
+                                                                              (const uint64_t*)h->bin_ent, h->cube);
     else if (h->apply_paper)
       k_bin_apply<3, 1, 4, true><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     else if (h->G.num_ra == 3 && h->G.num_va == 1 && B.s == 4)
@@ -572,7 +616,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     else
       k_bin_apply<0, 0, -1><<<n_wg, kApplyThreads, sm_ap, s>>>(h->G, B, start, cursor, h->bin_ent, h->cube);
     if ((rc = launch_check(h, "k_bin_apply"))) return rc;
-    if (wide && sl) {
+    if (wide && sl && !h->bin_wide) {
+      k_bin_log_wg<<<h->sms, 256, 0, s>>>(h->G, log_n, (const uint64_t*)h->bin_log, h->cube);
+      if ((rc = launch_check(h, "k_bin_log_wg"))) return rc;
+    } else if (wide && sl) {
       k_bin_log_w<<<h->sms, 256, 0, s>>>(h->G, log_n, (const uint64_t*)h->bin_log, h->cube);
       if ((rc = launch_check(h, "k_bin_log_w"))) return rc;
     } else if (h->bin_wc || sl) {   // the scatter's overflow log (usually empty: the kernel exits at once)
@@ -586,7 +633,7 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
 
 int update_all_passes(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint64_t n, cudaStream_t s) {
   ++h->tcalls;
-  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min)
+  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && binned_ok(h) && n >= h->bin_min)
     return update_binned(h, src, dst, n, s);
   const uint64_t W = h->cube_words;
   for (uint32_t p = 0; p < h->passes; ++p) {
@@ -734,10 +781,27 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     B.nblk = (uint32_t)h->sms * kBinMinBlocks;
     B.ncols = h->G.cs_words / h->G.wpc;
     // scatter tables ≤ 48 KiB (≥ 2 pairs per bin in an 8192-pair tile), word group ≤ 112 KiB
-    h->binnable = B.nbins <= 4096 && B.ncols <= 28672;
-    // auto (bin_min_pairs = 0): cubes up to 0.6 of L2 stay on the direct kernel, whose random accesses then
-    // hit L2 (C5 sweep, profiles/r01_sweep_c5.jsonl: r = 2 and 8-64 MiB cubes are faster direct)
-    if (!cfg->bin_min_pairs && h->cube_bytes <= 0.6 * (double)(h->l2_bytes > 0 ? h->l2_bytes : (126 << 20)))
+    h->bin_narrow_ok = B.nbins <= 4096 && B.ncols <= 28672;
+    // wide entries (LP << 6 | row mod 64) for any geometry with g ≥ 64, 256-2048 bins (cs, row >> 6) and
+    // two word groups in 128 KiB (Σc(i) ≤ 16384); the paper geometry keeps its constant-folded kernels
+    {
+      const uint32_t nbw = lg >= 6 ? h->G.n_cs << (lg - 6) : 0u;
+      const char* bw = std::getenv("CBAA_BIN_WIDE");
+      const char* bg = std::getenv("CBAA_BIN_WIDE_GEN");
+      h->bin_gen_ok = lg >= 6 && nbw >= 256 && nbw <= 2048 && B.ncols <= 16384 && h->G.narr <= CBAA_MAX_ARRAYS &&
+                      !(bw && bw[0] == '0') && !(bg && bg[0] == '0');
+    }
+    h->binnable = h->bin_narrow_ok || h->bin_gen_ok;
+    // generic wide entries unless the 32-bit entries already keep 5 row bits (r ≥ 5: one word group per
+    // bin, 4-B entries), which measured faster (profiles/r02_wide_generic.jsonl)
+    // (CBAA_BIN_WIDE_GEN=2 forces them wherever they fit: tests and A/Bs)
+    const char* bgf = std::getenv("CBAA_BIN_WIDE_GEN");
+    h->bin_gen_pref = h->bin_gen_ok && (!h->bin_narrow_ok || cfg->r < 5 || (bgf && bgf[0] == '2'));
+    // auto (bin_min_pairs = 0): cubes up to 0.6 of L2 stay on the direct kernel when only 32-bit entries
+    // with < 4 row bits are available (r < 4: runs of ~1-2 entries per tile; profiles/r02_wide_generic.jsonl:
+    // r = 2, g ≤ 2048 is faster direct); with wide entries or r ≥ 4 the binned path wins for every cube size
+    if (!cfg->bin_min_pairs && h->cube_bytes <= 0.6 * (double)(h->l2_bytes > 0 ? h->l2_bytes : (126 << 20)) &&
+        !(h->bin_gen_pref || (h->bin_narrow_ok && cfg->r >= 4)))
       h->binnable = 0;
     const char* bm = std::getenv("CBAA_BIN_MIN");
     h->bin_min = cfg->bin_min_pairs ? cfg->bin_min_pairs
@@ -784,17 +848,21 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
         // wide entries for the paper configuration (r = 4, g = 4096): CBAA_BIN_WIDE=0 keeps 32-bit entries
         const char* bw = std::getenv("CBAA_BIN_WIDE");
         h->bin_wide = pp && g.r == 4 && g.g == 4096 && !(bw && bw[0] == '0');
+        h->bin_wide_gen = !h->bin_wide && h->bin_gen_pref;
         BinGeo& W = h->BW;
         W.s = 6;
-        W.bpc_log2 = 6;
-        W.nbins = h->G.n_cs << 6;
+        W.bpc_log2 = lg >= 6 ? lg - 6 : 0;
+        W.nbins = h->G.n_cs << W.bpc_log2;
         W.nblk = B.nblk;
         W.ncols = B.ncols;
-        cudaFuncSetAttribute(k_bin_scatter_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmem);
-        cudaFuncSetAttribute(k_bin_scatter_w<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(k_bin_scatter_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWScatterSmemPrefix);
-        cudaFuncSetAttribute(k_bin_scatter_w<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        set_wscatter_attrs<-1>();
+        set_wscatter_attrs<256>();
+        set_wscatter_attrs<512>();
+        set_wscatter_attrs<1024>();
+        set_wscatter_attrs<2048>();
         cudaFuncSetAttribute(k_bin_apply_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
+        cudaFuncSetAttribute(k_bin_apply_wg<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
+        cudaFuncSetAttribute(k_bin_apply_wg<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
       }
       cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
       cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
@@ -1614,14 +1682,17 @@ uint32_t cbaa_update_passes(const cbaa_handle* h) { return h ? h->passes : 0; }
 int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t buflen) {
   if (!h || !buf || !buflen) return CBAA_E_ARG;
   std::string p;
-  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && h->binnable && n >= h->bin_min) {
+  if (h->cfg.update_mode == CBAA_UPDATE_BINNED && binned_ok(h) && n >= h->bin_min) {
     const bool prefix = h->cfg.direction == CBAA_DIR_INNER_PREFIX;
-    const bool wide = h->bin_wide && !h->bin_wc;
+    const bool wide = (h->bin_wide || h->bin_wide_gen) && !h->bin_wc;
+    const bool gen = wide && !h->bin_wide;
     const uint32_t samp = ((!prefix || wide) && !h->bin_wc) ? h->bin_sample_log2 : 0u;
     const bool sampled = samp && std::min(n, h->bin_chunk) >= h->bin_sample_min;
-    p = std::string(wide ? "binned-wide " : "binned ") + (sampled ? "k_bin_sample" : "k_bin_count") + " k_bin_starts " +
+    p = std::string(gen ? "binned-wide-generic " : wide ? "binned-wide " : "binned ") +
+        (sampled ? "k_bin_sample" : "k_bin_count") + " k_bin_starts " +
         (wide ? "k_bin_scatter_w" : h->bin_wc ? "k_bin_wc" : "k_bin_scatter") + " " +
-        (wide ? "k_bin_apply_w+k_bin_log_w" : "k_bin_apply+k_bin_log") + (wide ? " entry_bytes=8" : " entry_bytes=4");
+        (gen ? "k_bin_apply_wg+k_bin_log_wg" : wide ? "k_bin_apply_w+k_bin_log_w" : "k_bin_apply+k_bin_log") +
+        (wide ? " entry_bytes=8" : " entry_bytes=4") + (gen ? " bins=" + std::to_string(h->BW.nbins) : "");
   } else {
     p = "direct k_update passes=" + std::to_string(h->passes);
   }
