@@ -624,7 +624,7 @@ constexpr size_t kWApplySmem = 2 * 16384 * 4;                                   
 // PREFIX: raw on-wire pairs, classified by the inner prefixes (a0) with the two 8 KiB bitmaps
 // staged in shared memory; pairs with zero or two inner endpoints are skipped and counted here (every
 // pair passes through this kernel, so the bin regions can still come from a sample).
-// NB < 0: the paper geometry (r = 4, g = 4096: 1024 bins, shifts and masks as immediates); NB = 256..2048:
+// NB < 0: the paper geometry (r = 4, g = 4096: 1024 bins, shifts and masks as immediates); NB = 256..4096:
 // any geometry with g ≥ 64 whose 2^r·g/64 bins number NB (run-time r and g).  Rank key of a pair:
 // bin << (32 − log2 NB) | row mod 64 << (26 − log2 NB) | rank in the tile (the paper's cs << 28 | row << 16
 // | rank when NB = 1024).

@@ -572,8 +572,10 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
         launch_wscatter<512>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
       else if (B.nbins == 1024)
         launch_wscatter<1024>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
-      else
+      else if (B.nbins == 2048)
         launch_wscatter<2048>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
+      else
+        launch_wscatter<4096>(prefix, h->G, B.nblk, s, a, b, m, per, vec, cursor, ent, start, log_n, lgw, sk, h->scatter_pf);
     } else if (h->bin_wc) {   // write-combining scatter (CBAA_BIN_SCATTER=wc), one CTA per SM
       const uint32_t nw = (uint32_t)h->sms;
       const uint64_t per_w = (((m + nw - 1) / nw) + 3) & ~3ull;
@@ -788,7 +790,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       const uint32_t nbw = lg >= 6 ? h->G.n_cs << (lg - 6) : 0u;
       const char* bw = std::getenv("CBAA_BIN_WIDE");
       const char* bg = std::getenv("CBAA_BIN_WIDE_GEN");
-      h->bin_gen_ok = lg >= 6 && nbw >= 256 && nbw <= 2048 && B.ncols <= 16384 && h->G.narr <= CBAA_MAX_ARRAYS &&
+      h->bin_gen_ok = lg >= 6 && nbw >= 256 && nbw <= 4096 && B.ncols <= 16384 && h->G.narr <= CBAA_MAX_ARRAYS &&
                       !(bw && bw[0] == '0') && !(bg && bg[0] == '0');
     }
     h->binnable = h->bin_narrow_ok || h->bin_gen_ok;
@@ -860,6 +862,7 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
         set_wscatter_attrs<512>();
         set_wscatter_attrs<1024>();
         set_wscatter_attrs<2048>();
+        set_wscatter_attrs<4096>();
         cudaFuncSetAttribute(k_bin_apply_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
         cudaFuncSetAttribute(k_bin_apply_wg<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
         cudaFuncSetAttribute(k_bin_apply_wg<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
