@@ -1003,6 +1003,61 @@ __global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_wg(const __grid
   }
 }
 
+// Per-array apply of the wide entries (k_bin_scatter_w<·, NB>) when the word groups of all arrays do not
+// fit shared memory together (Σc(i) > 16384, e.g. cbn = 14: 512 KiB) but each array's do (c(a) ≤ 16384):
+// CTA (b, a) = blockIdx (b·narr + a) keeps the two word groups of array a only (≤ 128 KiB) and walks all of
+// bin b's entries, setting one bit per entry; the narr CTAs of a bin are adjacent, so the entries come from
+// DRAM once and from L2 for the others.  The cube is the same OR of bits.
+__global__ void __launch_bounds__(kWApplyThreads, 1) k_bin_apply_wa(const __grid_constant__ Geo G,
+                                                                   const uint32_t* __restrict__ start,
+                                                                   const uint32_t* __restrict__ end,
+                                                                   const uint64_t* __restrict__ entries,
+                                                                   uint32_t* __restrict__ cube) {
+  extern __shared__ uint32_t sub[];
+  const uint32_t sbase = pin(smem_addr(sub));
+  const uint32_t narr = G.narr, bpl = G.wpc_log2 - 1u;
+  const uint32_t b = blockIdx.x / narr, a = blockIdx.x - b * narr;
+  const uint32_t cs = b >> bpl, wq = b & ((1u << bpl) - 1u);
+  const uint32_t cols = G.ncols[a], L = G.L;
+  for (uint32_t i = threadIdx.x; i < 2 * cols / 4; i += kWApplyThreads)
+    reinterpret_cast<uint4*>(sub)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const bool ra = a < G.num_ra;
+  const uint32_t sh = ra ? G.sh[a] : 0u, cm = G.colmask[a], seed = ra ? 0u : G.va_seeds[a - G.num_ra];
+  const uint32_t P0 = start[b], E0 = min(end[b * kCurStride], start[b + 1]);
+  const uint64_t* __restrict__ ent = entries + P0;
+  const uint32_t len = E0 - P0;
+  auto set_bit = [&](uint64_t e) {
+    const uint32_t lp = (uint32_t)(e >> 6), r6 = (uint32_t)e & 63u;
+    const uint32_t c = ra ? (uint32_t)((((uint64_t)lp << L) | lp) >> sh) & cm : mix32(lp ^ seed) & cm;
+    const uint32_t adr = sbase + (r6 >> 5) * (4u * cols) + 4u * c, bit = 1u << (r6 & 31u);
+    if (!(lds(adr) & bit)) reds_or(adr, bit);
+  };
+  constexpr uint32_t kStep = kApplyUnroll * kWApplyThreads;
+  uint64_t e[kApplyUnroll];
+  uint32_t p = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kApplyUnroll; ++u) e[u] = p + u * kWApplyThreads < len ? ent[p + u * kWApplyThreads] : 0ull;
+  while (p < len) {
+    const uint32_t pn = p + kStep;
+    uint64_t en[kApplyUnroll];
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) en[u] = pn + u * kWApplyThreads < len ? ent[pn + u * kWApplyThreads] : 0ull;
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u)
+      if (p + u * kWApplyThreads < len) set_bit(e[u]);
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) e[u] = en[u];
+    p = pn;
+  }
+  __syncthreads();
+  uint32_t* cw = cube + (uint64_t)cs * G.cs_words + G.arr_off[a] + 2u * wq;
+  for (uint32_t i = threadIdx.x; i < cols; i += kWApplyThreads) {
+    const uint32_t v0 = sub[i], v1 = sub[cols + i];
+    if (v0 | v1) red_or64(reinterpret_cast<unsigned long long*>(cw + (uint64_t)i * G.wpc), ((uint64_t)v1 << 32) | v0);
+  }
+}
+
 // Overflow log of the generic wide scatter: records bin << 48 | LP << 6 | row mod 64, applied with the
 // direct update's test-and-set.
 __global__ void k_bin_log_wg(const __grid_constant__ Geo G, const uint32_t* __restrict__ log_n,

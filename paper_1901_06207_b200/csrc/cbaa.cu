@@ -100,6 +100,7 @@ struct cbaa_handle {
   int bin_narrow_ok = 0;          // the 32-bit-entry kernels' tables fit (nbins ≤ 4096, Σc(i) ≤ 28672)
   int bin_gen_ok = 0;             // the generic wide kernels fit
   int bin_gen_pref = 0;           // ... and are preferred over the 32-bit-entry kernels
+  int bin_gen_per_array = 0;      // ... with one apply CTA per (bin, array): Σc(i) > 16384 (k_bin_apply_wa)
   BinGeo BW{};                    // bin geometry of the wide path
   uint32_t sample_ctas = 0;       // k_bin_sample grid (0: one CTA per SM; CBAA_SAMPLE_CTAS)
   uint32_t scatter_pf = 1 | 1u << 8;   // k_bin_scatter_w L2 prefetch: distance in tiles | issue point << 8 (CBAA_SCATTER_PF)
@@ -462,12 +463,18 @@ bool binned_ok(const cbaa_handle* h) {
   return h->binnable && (wide || h->bin_narrow_ok);
 }
 
+// the largest dynamic shared memory a kernel may request: the opt-in maximum less its static shared memory
+void set_dyn_smem_max(const void* f, int smax) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, f) == cudaSuccess)
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - (int)fa.sharedSizeBytes);
+}
+
 template <int NB>
-void set_wscatter_attrs() {
-  const uint32_t nb = NB < 0 ? (uint32_t)kWBins : (uint32_t)NB;
-  cudaFuncSetAttribute(k_bin_scatter_w<false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wscatter_smem(nb, false));
+void set_wscatter_attrs(int smax) {
+  set_dyn_smem_max((const void*)k_bin_scatter_w<false, NB>, smax);
   cudaFuncSetAttribute(k_bin_scatter_w<false, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaFuncSetAttribute(k_bin_scatter_w<true, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wscatter_smem(nb, true));
+  set_dyn_smem_max((const void*)k_bin_scatter_w<true, NB>, smax);
   cudaFuncSetAttribute(k_bin_scatter_w<true, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
@@ -603,7 +610,12 @@ int update_binned(cbaa_handle* h, const uint32_t* src, const uint32_t* dst, uint
     if (wide && h->bin_wide)
       k_bin_apply_w<<<B.nbins, kWApplyThreads, kWApplySmem, s>>>(h->G, start, cursor, (const uint64_t*)h->bin_ent,
                                                                  h->cube);
-    else if (wide && h->G.num_ra == 3 && h->G.num_va == 1)
+    else if (wide && h->bin_gen_per_array) {
+      uint32_t maxc = 0;
+      for (uint32_t q = 0; q < h->G.narr; ++q) maxc = std::max(maxc, h->G.ncols[q]);
+      k_bin_apply_wa<<<B.nbins * h->G.narr, kWApplyThreads, (size_t)maxc * 8, s>>>(h->G, start, cursor,
+                                                                                 (const uint64_t*)h->bin_ent, h->cube);
+    } else if (wide && h->G.num_ra == 3 && h->G.num_va == 1)
       k_bin_apply_wg<3, 1><<<B.nbins, kWApplyThreads, (size_t)B.ncols * 8, s>>>(h->G, B.ncols, start, cursor,
                                                                               (const uint64_t*)h->bin_ent, h->cube);
     else if (wide)
@@ -790,8 +802,11 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       const uint32_t nbw = lg >= 6 ? h->G.n_cs << (lg - 6) : 0u;
       const char* bw = std::getenv("CBAA_BIN_WIDE");
       const char* bg = std::getenv("CBAA_BIN_WIDE_GEN");
-      h->bin_gen_ok = lg >= 6 && nbw >= 256 && nbw <= 4096 && B.ncols <= 16384 && h->G.narr <= CBAA_MAX_ARRAYS &&
+      uint32_t maxc = 0;   // the largest array: its two word groups must fit 128 KiB for the per-array apply
+      for (uint32_t a = 0; a < h->G.narr; ++a) maxc = std::max(maxc, h->G.ncols[a]);
+      h->bin_gen_ok = lg >= 6 && nbw >= 256 && nbw <= 4096 && maxc <= 16384 && h->G.narr <= CBAA_MAX_ARRAYS &&
                       !(bw && bw[0] == '0') && !(bg && bg[0] == '0');
+      h->bin_gen_per_array = B.ncols > 16384;   // k_bin_apply_wa: one CTA per (bin, array)
     }
     h->binnable = h->bin_narrow_ok || h->bin_gen_ok;
     // generic wide entries unless the 32-bit entries already keep 5 row bits (r ≥ 5: one word group per
@@ -815,9 +830,13 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
     if (bc && std::strtoull(bc, nullptr, 10) > 0)
       h->bin_chunk = std::min<uint64_t>(1ull << 28, std::strtoull(bc, nullptr, 10));
     if (h->binnable) {
-      const int sm_cnt = (int)B.nbins * 4, sm_sc = (int)((3 * B.nbins + 1) * 4 + kBinTile * 6), sm_ap = (int)B.ncols * 4;
-      cudaFuncSetAttribute(k_bin_sample<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
-      cudaFuncSetAttribute(k_bin_sample<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      // every binned kernel may use up to the opt-in maximum of dynamic shared memory: the attribute is
+      // per function and process-wide, so a per-handle size would cap another handle's (larger) launches;
+      // the launch's own size still sets the occupancy
+      int smax = 0;
+      cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+      set_dyn_smem_max((const void*)k_bin_sample<false>, smax);
+      set_dyn_smem_max((const void*)k_bin_sample<true>, smax);
       const char* sp = std::getenv("CBAA_BIN_SAMPLE");
       if (sp) {
         const unsigned long v = std::strtoul(sp, nullptr, 10);
@@ -825,23 +844,22 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
       }
       const char* spm = std::getenv("CBAA_BIN_SAMPLE_MIN");
       if (spm) h->bin_sample_min = std::strtoull(spm, nullptr, 10);
-      cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
-      cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_cnt);
+      set_dyn_smem_max((const void*)k_bin_count<false>, smax);
+      set_dyn_smem_max((const void*)k_bin_count<true>, smax);
       const char* bs = std::getenv("CBAA_BIN_SCATTER");
       h->bin_wc = bs && std::strcmp(bs, "wc") == 0;
-      const int sm_wc = (int)wc_smem_bytes(B.nbins);
-      cudaFuncSetAttribute(k_bin_wc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
-      cudaFuncSetAttribute(k_bin_wc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_wc);
-      cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
-      cudaFuncSetAttribute(k_bin_scatter<false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      set_dyn_smem_max((const void*)k_bin_wc<false>, smax);
+      set_dyn_smem_max((const void*)k_bin_wc<true>, smax);
+      set_dyn_smem_max((const void*)k_bin_scatter<false, 0>, smax);
+      set_dyn_smem_max((const void*)k_bin_scatter<false, 4096>, smax);
+      set_dyn_smem_max((const void*)k_bin_scatter<false, -1>, smax);
       cudaFuncSetAttribute(k_bin_scatter<false, -1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sc);
+      set_dyn_smem_max((const void*)k_bin_scatter<true, 0>, smax);
       cudaFuncSetAttribute(k_bin_scatter<false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_scatter<false, 4096>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       cudaFuncSetAttribute(k_bin_scatter<true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(k_bin_apply<3, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
-      cudaFuncSetAttribute(k_bin_apply<3, 1, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      set_dyn_smem_max((const void*)k_bin_apply<3, 1, 4>, smax);
+      set_dyn_smem_max((const void*)k_bin_apply<3, 1, 4, true>, smax);
       {   // the paper's default configuration: k_bin_apply<3, 1, 4, true> with constants inlined
         const Geo& g = h->G;
         bool pp = g.num_ra == 3 && g.num_va == 1 && B.s == 4 && g.sh[0] == 44 && g.sh[1] == 34 && g.sh[2] == 24;
@@ -857,18 +875,20 @@ int cbaa_create_ext(const cbaa_config* cfg, int device, void* cube, uint64_t cub
         W.nbins = h->G.n_cs << W.bpc_log2;
         W.nblk = B.nblk;
         W.ncols = B.ncols;
-        set_wscatter_attrs<-1>();
-        set_wscatter_attrs<256>();
-        set_wscatter_attrs<512>();
-        set_wscatter_attrs<1024>();
-        set_wscatter_attrs<2048>();
-        set_wscatter_attrs<4096>();
-        cudaFuncSetAttribute(k_bin_apply_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
-        cudaFuncSetAttribute(k_bin_apply_wg<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
-        cudaFuncSetAttribute(k_bin_apply_wg<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWApplySmem);
+        set_wscatter_attrs<-1>(smax);
+        set_wscatter_attrs<256>(smax);
+        set_wscatter_attrs<512>(smax);
+        set_wscatter_attrs<1024>(smax);
+        set_wscatter_attrs<2048>(smax);
+        set_wscatter_attrs<4096>(smax);
+        set_dyn_smem_max((const void*)k_bin_apply_w, smax);
+        set_dyn_smem_max((const void*)k_bin_apply_wg<3, 1>, smax);
+        set_dyn_smem_max((const void*)k_bin_apply_wg<0, 0>, smax);
+        set_dyn_smem_max((const void*)k_bin_apply_wa, smax);
       }
-      cudaFuncSetAttribute(k_bin_apply<3, 1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
-      cudaFuncSetAttribute(k_bin_apply<0, 0, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_ap);
+      set_dyn_smem_max((const void*)k_bin_apply<3, 1, -1>, smax);
+      set_dyn_smem_max((const void*)k_bin_apply<0, 0, -1>, smax);
+      (void)cudaGetLastError();   // an attribute the device refused must not surface at a later launch check
     }
   }
   int occ = 0;
@@ -1694,7 +1714,8 @@ int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t bufle
     p = std::string(gen ? "binned-wide-generic " : wide ? "binned-wide " : "binned ") +
         (sampled ? "k_bin_sample" : "k_bin_count") + " k_bin_starts " +
         (wide ? "k_bin_scatter_w" : h->bin_wc ? "k_bin_wc" : "k_bin_scatter") + " " +
-        (gen ? "k_bin_apply_wg+k_bin_log_wg" : wide ? "k_bin_apply_w+k_bin_log_w" : "k_bin_apply+k_bin_log") +
+        (gen ? (h->bin_gen_per_array ? "k_bin_apply_wa+k_bin_log_wg" : "k_bin_apply_wg+k_bin_log_wg")
+             : wide ? "k_bin_apply_w+k_bin_log_w" : "k_bin_apply+k_bin_log") +
         (wide ? " entry_bytes=8" : " entry_bytes=4") + (gen ? " bins=" + std::to_string(h->BW.nbins) : "");
   } else {
     p = "direct k_update passes=" + std::to_string(h->passes);

@@ -23,8 +23,9 @@ def plan(cb, n):
 
 
 # (r, g, cbn) → wide bins 2^r·g/64: 256 (4, 1024), 512 (2, 8192), 1024 (6, 1024), 2048 (4, 8192), (6, 2048),
-# 4096 (6, 4096)
-GEOS = [(4, 1024, 10), (2, 8192, 12), (6, 1024, 12), (4, 8192, 12), (6, 2048, 10), (2, 4096, 10), (6, 4096, 12)]
+# 4096 (6, 4096); cbn = 14: Σc(i) > 16384, one apply CTA per (bin, array) (k_bin_apply_wa)
+GEOS = [(4, 1024, 10), (2, 8192, 12), (6, 1024, 12), (4, 8192, 12), (6, 2048, 10), (2, 4096, 10), (6, 4096, 12),
+        (4, 2048, 14), (6, 1024, 14)]
 
 
 @pytest.fixture
