@@ -186,7 +186,9 @@ int cbaa_reset(cbaa_handle* h, cbaa_stream stream);
  * log, so the cube never depends on the sample.  Environment knobs read at
  * cbaa_create (tests, A/B): CBAA_BIN_SAMPLE (log2 of the sampling period,
  * 0 = exact count), CBAA_BIN_SAMPLE_MIN, CBAA_BIN_SCATTER=wc (write-combining
- * scatter, exact count), CBAA_BIN_CHUNK, CBAA_BIN_MIN.  Updates accumulate until cbaa_reset; calls on
+ * scatter, exact count), CBAA_BIN_CHUNK, CBAA_BIN_MIN, CBAA_BIN_WIDE=0 (32-bit
+ * entries only), CBAA_BIN_WIDE_GEN=0/2 (generic wide entries off / wherever
+ * they fit), CBAA_SCATTER_PF (the scatter's L2 prefetch; 0 = off).  Updates accumulate until cbaa_reset; calls on
  * one handle must be stream-ordered with its detect/merge/reset.  Any 4-byte
  * alignment is accepted (16-B aligned arrays take the vector path).  Async on
  * stream. */
@@ -383,7 +385,9 @@ int cbaa_update_phase_ms(cbaa_handle* h, double* ms, int cap, uint64_t* calls);
 
 /* The kernels a cbaa_update call of n pairs would launch, per phase, as one NUL-terminated line written
  * into buf (buflen bytes, truncated): "binned-wide k_bin_sample k_bin_starts k_bin_scatter_w
- * k_bin_apply_w+k_bin_log_w entry_bytes=8", "binned ... entry_bytes=4", or "direct k_update passes=P".
+ * k_bin_apply_w+k_bin_log_w entry_bytes=8" (paper geometry), "binned-wide-generic ... k_bin_apply_wg (or
+ * k_bin_apply_wa, one CTA per bin and array)+k_bin_log_wg entry_bytes=8 bins=B" (other geometries with
+ * 256-4096 wide bins), "binned ... entry_bytes=4", or "direct k_update passes=P".
  * Host only, no GPU work; CBAA_E_ARG if h or buf is null (bench evidence: which kernel is dominant). */
 int cbaa_update_plan(const cbaa_handle* h, uint64_t n, char* buf, uint64_t buflen);
 
