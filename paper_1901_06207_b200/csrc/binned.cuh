@@ -617,8 +617,6 @@ __host__ __device__ constexpr uint32_t ilog2c(uint32_t v) { return v <= 1 ? 0 : 
 constexpr size_t wscatter_smem(uint32_t nbins, bool prefix) {
   return (size_t)kBinTile * 8 + (3 * nbins + 1) * 4 + (prefix ? 4096 * 4 : 0);
 }
-constexpr size_t kWScatterSmem = wscatter_smem(kWBins, false);
-constexpr size_t kWScatterSmemPrefix = wscatter_smem(kWBins, true);
 constexpr size_t kWApplySmem = 2 * 16384 * 4;                                   // two word groups, 128 KiB
 
 // PREFIX: raw on-wire pairs, classified by the inner prefixes (a0) with the two 8 KiB bitmaps
